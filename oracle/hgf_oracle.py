@@ -1,0 +1,376 @@
+"""HGF oracle: a plain, slow, float64 CPU implementation of what the hot path computes.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this module.
+The product path (``paper_1803_00005_b200``) never imports it, and this module
+imports nothing from the product path: the two share no code, headers, tables or
+constants.  Inputs come from ``synth`` (seeded generators with none of the
+method's arithmetic).
+
+Paper: Dai et al., "Hardware-Efficient Guided Image Filtering for Multi-Label
+Problem", CVPR 2018 (arXiv 1803.00005).  ``P:n`` below is line n of
+``PAPER.md`` (the LaTeX source); equation numbers follow SURVEY.md's list
+(Eq1 P:36 ... Eq16).
+
+Readings of the paper taken here (all listed in DESIGN.md §3):
+  F1  alpha^0_00 = -lambda^-1 (lambda + G_00)^-1   (printed: -(lambda+G_00)^-1)
+  F2  Eq11 first case carries gamma (gamma F + alpha), as Eq4 does (P:145 vs P:315)
+  F3  Eq13 W_k = lambda^-1 G_{k,n+1} + sum_{i,j=0..n} alpha_ij G_ki G_{j,n+1}, k = 0..n
+  F4  Eq5's I_{ki} read as G_{ki}
+  F5  F^kappa_ij = u_i v_j, u_i = sum_{m<k} alpha_im G_mk, v_j = sum_{m<k} alpha_mj G_km
+  F6  windows clipped at the image border, exact counts N_p (A(X) = B(X)/B(G_0))
+  F7  B is a box SUM ("equal to the sum of its neighboring pixels"): lambda is against sums
+  F9  HGF penalises the intercept w(0) (Eq7); GF (§5.1) does not (Eq15)
+  F14 WTA ties resolve to the lowest label index
+  F18 Eq8 reads Z(q) = 1/|Omega_q| sum_{p in Omega_q} (sum_i w_p(i) G_i(q) + w_p(0))
+
+Parity pins for every function live in tests/test_oracle_*.py (run with -m "not gpu").
+No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "box_sum", "box_count", "box_mean", "box_sum_brute",
+    "poly_guidance", "gram_planes", "alpha_recursion", "weights_eq13",
+    "hgf_filter", "hgf_filter_brute", "gf_he",
+    "wta", "aggregate_wta", "pack_keys", "unpack_keys",
+]
+
+MODE_HGF = "hgf"
+MODE_GF = "gf"
+
+
+# --------------------------------------------------------------------------
+# Box filter (§4.3; Prop 2)
+# --------------------------------------------------------------------------
+def _sat(X: np.ndarray) -> np.ndarray:
+    """Summed-area table (Crow 1984, cited P:342): S[..., y, x] = sum of X over rows < y, cols < x."""
+    X = np.asarray(X, dtype=np.float64)
+    H, W = X.shape[-2:]
+    S = np.zeros(X.shape[:-2] + (H + 1, W + 1), dtype=np.float64)
+    S[..., 1:, 1:] = X.cumsum(axis=-2).cumsum(axis=-1)
+    return S
+
+
+def box_sum(X: np.ndarray, r: int) -> np.ndarray:
+    """B(X)(p) = sum_{q in Omega_p} X(q), Omega_p the (2r+1)^2 box clipped to the image (F6, F7).
+
+    Works on any leading shape; the last two axes are (H, W).
+    """
+    X = np.asarray(X, dtype=np.float64)
+    H, W = X.shape[-2:]
+    S = _sat(X)
+    y0 = np.clip(np.arange(H) - r, 0, H)
+    y1 = np.clip(np.arange(H) + r + 1, 0, H)
+    x0 = np.clip(np.arange(W) - r, 0, W)
+    x1 = np.clip(np.arange(W) + r + 1, 0, W)
+    return (S[..., y1[:, None], x1[None, :]] - S[..., y0[:, None], x1[None, :]]
+            - S[..., y1[:, None], x0[None, :]] + S[..., y0[:, None], x0[None, :]])
+
+
+def box_sum_brute(X: np.ndarray, r: int) -> np.ndarray:
+    """Explicit double loop over every clipped window (used to pin box_sum; tiny inputs only)."""
+    X = np.asarray(X, dtype=np.float64)
+    H, W = X.shape[-2:]
+    out = np.zeros_like(X)
+    for y in range(H):
+        for x in range(W):
+            out[..., y, x] = X[..., max(0, y - r):min(H, y + r + 1), max(0, x - r):min(W, x + r + 1)].sum(axis=(-2, -1))
+    return out
+
+
+def box_count(H: int, W: int, r: int) -> np.ndarray:
+    """N_p = |Omega_p| = B(G_0)(p) with G_0 the ones image."""
+    ny = np.minimum(np.arange(H) + r, H - 1) - np.maximum(np.arange(H) - r, 0) + 1
+    nx = np.minimum(np.arange(W) + r, W - 1) - np.maximum(np.arange(W) - r, 0) + 1
+    return (ny[:, None] * nx[None, :]).astype(np.float64)
+
+
+def box_mean(X: np.ndarray, r: int) -> np.ndarray:
+    """Average operator A(X) = B(X) / B(G_0) (Eq14)."""
+    X = np.asarray(X, dtype=np.float64)
+    return box_sum(X, r) / box_count(X.shape[-2], X.shape[-1], r)
+
+
+# --------------------------------------------------------------------------
+# Polynomial guidance (§4.2; P:630 uses j <= 2)
+# --------------------------------------------------------------------------
+def poly_guidance(I: np.ndarray, d: int) -> np.ndarray:
+    """G_{(i-1)d+j} = I_i^j, i = 1..m, j = 1..d, stacked channel-major.
+
+    I: (m, H, W).  Returns (m*d, H, W) float64.  Powers by repeated multiplication.
+    """
+    I = np.asarray(I, dtype=np.float64)
+    if I.ndim == 2:
+        I = I[None]
+    if d < 1:
+        raise ValueError("degree d must be >= 1")
+    m = I.shape[0]
+    G = np.empty((m * d,) + I.shape[1:], dtype=np.float64)
+    for i in range(m):
+        t = np.ones(I.shape[1:], dtype=np.float64)
+        for j in range(d):
+            t = t * I[i]
+            G[i * d + j] = t
+    return G
+
+
+# --------------------------------------------------------------------------
+# Gram planes G_ij = B(G_i G_j) (Prop 2; Eq12)
+# --------------------------------------------------------------------------
+def gram_planes(G: np.ndarray, r: int, Y: np.ndarray | None = None):
+    """Return (Gram, Gy) where, with G_0 = ones:
+
+    Gram[i, j] = B(G_i G_j) for 0 <= i, j <= n   (shape (n+1, n+1, H, W))
+    Gy[j]      = B(G_j Y) = G_{j,n+1}            (shape (n+1, H, W)), if Y is given (G_{n+1} = Y)
+    """
+    G = np.asarray(G, dtype=np.float64)
+    n, H, W = G.shape
+    ext = np.concatenate([np.ones((1, H, W)), G], axis=0)
+    Gram = np.empty((n + 1, n + 1, H, W))
+    for i in range(n + 1):
+        for j in range(i, n + 1):
+            Gram[i, j] = box_sum(ext[i] * ext[j], r)
+            Gram[j, i] = Gram[i, j]
+    Gy = None
+    if Y is not None:
+        Y = np.asarray(Y, dtype=np.float64)
+        Gy = box_sum(ext * Y[None], r)
+    return Gram, Gy
+
+
+# --------------------------------------------------------------------------
+# Proposition 1: the hardware-efficient inverse (Eq4, plane form Eq11)
+# --------------------------------------------------------------------------
+def alpha_recursion(Gram: np.ndarray, lam: float) -> np.ndarray:
+    """alpha such that (lam E + sum_i c_i c_i^T)^-1 = lam^-1 E + sum_ij alpha_ij c_i c_j^T (Eq4).
+
+    Gram: (K, K, ...) with Gram[i, j] = c_i^T c_j (any trailing per-pixel shape: the plane form).
+    Runs kappa = 1..K-1 from alpha^0_00 (F1), each step reading only alpha^{kappa-1}.
+    """
+    Gram = np.asarray(Gram, dtype=np.float64)
+    K = Gram.shape[0]
+    inv_lam = 1.0 / lam
+    alpha = np.zeros_like(Gram)
+    # F1: alpha^0_00 = -lambda^-1 (lambda + G_00)^-1
+    alpha[0, 0] = -inv_lam / (lam + Gram[0, 0])
+    for k in range(1, K):
+        prev = alpha[:k, :k].copy()                                          # alpha^{kappa-1}
+        u = np.einsum("im...,m...->i...", prev, Gram[:k, k])                # u_i = sum_m alpha_im G_m,kappa
+        v = np.einsum("mj...,m...->j...", prev, Gram[k, :k])                # v_j = sum_m alpha_mj G_kappa,m
+        quad = np.einsum("mn...,m...,n...->...", prev, Gram[k, :k], Gram[:k, k])
+        gamma = -1.0 / (1.0 + inv_lam * Gram[k, k] + quad)                  # gamma^kappa
+        alpha[:k, :k] = gamma * u[:, None] * v[None, :] + prev              # i<k, j<k: gamma F + alpha (F2)
+        alpha[:k, k] = inv_lam * gamma * u                                   # i<k, j=k
+        alpha[k, :k] = inv_lam * gamma * v                                   # i=k, j<k
+        alpha[k, k] = inv_lam * inv_lam * gamma                              # i=j=k
+    return alpha
+
+
+def weights_eq13(alpha: np.ndarray, Gram: np.ndarray, Gy: np.ndarray, lam: float) -> np.ndarray:
+    """Eq13 / Eq5 (F3, F4): W_k = lam^-1 G_{k,n+1} + sum_{i,j} alpha_ij G_ki G_{j,n+1}, k = 0..n."""
+    t = np.einsum("ij...,j...->i...", alpha, Gy)           # sum_j alpha_ij G_{j,n+1}
+    return Gy / lam + np.einsum("ki...,i...->k...", Gram, t)
+
+
+# --------------------------------------------------------------------------
+# The filter (Eq6-8, Eq14; GF mode Eq15-16)
+# --------------------------------------------------------------------------
+def _aggregate(W: np.ndarray, G: np.ndarray, r: int) -> np.ndarray:
+    """Eq14: Z = sum_{i=1..n} A(W_i) G_i + A(W_0)  (== Eq8)."""
+    AW = box_mean(W, r)
+    return AW[0] + np.einsum("i...,i...->...", AW[1:], G)
+
+
+def _solve_batched(M: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """w_p = M_p^-1 b_p for every pixel.  M: (K, K, H, W); b: (K, H, W) or (K, L, H, W)."""
+    K = M.shape[0]
+    Mp = np.moveaxis(M, (0, 1), (-2, -1))                      # (H, W, K, K)
+    if b.ndim == 3:
+        bp = np.moveaxis(b, 0, -1)[..., None]                  # (H, W, K, 1)
+        return np.moveaxis(np.linalg.solve(Mp, bp)[..., 0], -1, 0)
+    bp = np.moveaxis(b, (0, 1), (-2, -1))                      # (H, W, K, L)
+    return np.moveaxis(np.linalg.solve(Mp, bp), (-2, -1), (0, 1))
+
+
+def hgf_weights(G: np.ndarray, Y: np.ndarray, lam: float, r: int, mode: str = MODE_HGF,
+                method: str = "solve") -> np.ndarray:
+    """Per-pixel coefficients w_p = (w_p(0), ..., w_p(n)) (shape (n+1, H, W) or (n+1, L, H, W)).
+
+    mode "hgf": Eq7 -> Eq2: w = (lam E + X^T X)^-1 X^T c_{n+1}; all n+1 coefficients penalised.
+    mode "gf":  Eq15/16: centred slopes (lam E + X'^T X')^-1 X'^T c', w(0) = mean(c) - w^T mean(x).
+    method "solve": a dense solve per pixel (the plain definition).
+    method "paper": Prop 1 recursion (alpha) + Eq13 / Eq5 weights (the paper's scheme).
+    Y may be (H, W) or a stack (L, H, W) of slices.
+    """
+    G = np.asarray(G, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    n, H, W = G.shape
+    Gram, _ = gram_planes(G, r)
+    ext = np.concatenate([np.ones((1, H, W)), G], axis=0)
+    if Y.ndim == 2:
+        Gy = box_sum(ext * Y[None], r)                          # (n+1, H, W)
+    else:
+        Gy = box_sum(ext[:, None] * Y[None], r)                 # (n+1, L, H, W)
+    if mode == MODE_HGF:
+        if method == "solve":
+            M = Gram + lam * np.eye(n + 1)[:, :, None, None]
+            return _solve_batched(M, Gy)
+        if method == "paper":
+            alpha = alpha_recursion(Gram, lam)
+            if Gy.ndim == 3:
+                return weights_eq13(alpha, Gram, Gy, lam)
+            return np.stack([weights_eq13(alpha, Gram, Gy[:, l], lam) for l in range(Gy.shape[1])], axis=1)
+        raise ValueError(method)
+    if mode == MODE_GF:
+        N = Gram[0, 0]
+        mu = Gram[0, 1:] / N                                    # x-bar
+        # centred Gram G'_ij = c'_i^T c'_j = G_ij - N mu_i mu_j  (i, j = 1..n)
+        Gc = Gram[1:, 1:] - N * mu[:, None] * mu[None, :]
+        ybar = Gy[0] / N                                        # c_{n+1} bar
+        if Gy.ndim == 3:
+            cc = Gy[1:] - N * mu * ybar                         # X'^T c'_{n+1}
+        else:
+            cc = Gy[1:] - N * mu[:, None] * ybar[None]
+        if method == "solve":
+            M = Gc + lam * np.eye(n)[:, :, None, None]
+            ws = _solve_batched(M, cc)
+        elif method == "paper":
+            alpha = alpha_recursion(Gc, lam)                    # same technique on Eq16
+            if cc.ndim == 3:
+                ws = weights_eq13(alpha, Gc, cc, lam)
+            else:
+                ws = np.stack([weights_eq13(alpha, Gc, cc[:, l], lam) for l in range(cc.shape[1])], axis=1)
+        else:
+            raise ValueError(method)
+        if ws.ndim == 3:
+            w0 = ybar - np.einsum("i...,i...->...", ws, mu)
+        else:
+            w0 = ybar - np.einsum("il...,i...->l...", ws, mu)
+        return np.concatenate([w0[None], ws], axis=0)
+    raise ValueError(mode)
+
+
+def hgf_filter(I: np.ndarray, Y: np.ndarray, lam: float, r: int, d: int, mode: str = MODE_HGF,
+               method: str = "solve") -> np.ndarray:
+    """Z = HGF(Y; guidance synthesised from I) (Fig 2): guidance -> Gram -> w -> Eq14.
+
+    I: (m, H, W) raw guide; Y: (H, W) slice or (L, H, W) stack.  Returns Z with Y's shape.
+    """
+    G = poly_guidance(I, d)
+    w = hgf_weights(G, Y, lam, r, mode=mode, method=method)
+    if w.ndim == 3:
+        return _aggregate(w, G, r)
+    return np.stack([_aggregate(w[:, l], G, r) for l in range(w.shape[1])], axis=0)
+
+
+def hgf_filter_brute(I: np.ndarray, Y: np.ndarray, lam: float, r: int, d: int,
+                     mode: str = MODE_HGF) -> np.ndarray:
+    """Explicit per-window regression + explicit Eq8 aggregation (tiny inputs only).
+
+    For each p: gather X_p = [1, G_1..G_n] over the clipped window, solve the ridge normal
+    equations by LU (np.linalg.solve); then Z(q) = mean_{p in Omega_q} (w_p(0) + sum_i w_p(i) G_i(q)).
+    """
+    G = poly_guidance(I, d)
+    Y = np.asarray(Y, dtype=np.float64)
+    n, H, W = G.shape
+    w = np.zeros((n + 1, H, W))
+    for y in range(H):
+        for x in range(W):
+            ys = slice(max(0, y - r), min(H, y + r + 1))
+            xs = slice(max(0, x - r), min(W, x + r + 1))
+            cols = [np.ones(G[0, ys, xs].size)] + [G[i, ys, xs].ravel() for i in range(n)]
+            X = np.stack(cols, axis=1)
+            c = Y[ys, xs].ravel()
+            if mode == MODE_HGF:
+                w[:, y, x] = np.linalg.solve(lam * np.eye(n + 1) + X.T @ X, X.T @ c)
+            else:
+                Xc = X[:, 1:] - X[:, 1:].mean(axis=0)[None]
+                cc = c - c.mean()
+                ws = np.linalg.solve(lam * np.eye(n) + Xc.T @ Xc, Xc.T @ cc)
+                w[1:, y, x] = ws
+                w[0, y, x] = c.mean() - ws @ X[:, 1:].mean(axis=0)
+    Z = np.zeros((H, W))
+    for y in range(H):
+        for x in range(W):
+            acc, cnt = 0.0, 0
+            for py in range(max(0, y - r), min(H, y + r + 1)):
+                for px in range(max(0, x - r), min(W, x + r + 1)):
+                    acc += w[0, py, px] + sum(w[i + 1, py, px] * G[i, y, x] for i in range(n))
+                    cnt += 1
+            Z[y, x] = acc / cnt
+    return Z
+
+
+def gf_he(I: np.ndarray, p: np.ndarray, eps: np.ndarray | float, r: int) -> np.ndarray:
+    """He et al.'s guided filter closed form (means; gray or colour guide), used to pin GF mode.
+
+    a = (Sigma_p + eps U)^-1 cov_p(I, p), b = mean(p) - a^T mean(I), q = mean(a)^T I + mean(b).
+    eps may be a per-pixel plane (GF mode's lambda against sums gives eps_p = lambda / N_p).
+    """
+    I = np.asarray(I, dtype=np.float64)
+    if I.ndim == 2:
+        I = I[None]
+    p = np.asarray(p, dtype=np.float64)
+    m, H, W = I.shape
+    mI = box_mean(I, r)
+    mp = box_mean(p, r)
+    cov = box_mean(I * p[None], r) - mI * mp[None]
+    Sig = np.empty((m, m, H, W))
+    for i in range(m):
+        for j in range(m):
+            Sig[i, j] = box_mean(I[i] * I[j], r) - mI[i] * mI[j]
+    eps = np.broadcast_to(np.asarray(eps, dtype=np.float64), (H, W))
+    Sig = Sig + np.eye(m)[:, :, None, None] * eps[None, None]
+    a = _solve_batched(Sig, cov)
+    b = mp - np.einsum("i...,i...->...", a, mI)
+    return np.einsum("i...,i...->...", box_mean(a, r), I) + box_mean(b, r)
+
+
+# --------------------------------------------------------------------------
+# Winner-takes-all (§1) and the packed keys of the label-sharded merge
+# --------------------------------------------------------------------------
+def wta(Z: np.ndarray) -> np.ndarray:
+    """label(q) = min{ l : Z_l(q) = min_k Z_k(q) } (F14).  Z: (L, H, W) -> int32 (H, W)."""
+    Z = np.asarray(Z)
+    L = Z.shape[0]
+    best = Z[0].copy()
+    lab = np.zeros(Z.shape[1:], dtype=np.int32)
+    for l in range(1, L):                       # strict '<' keeps the lowest index on ties
+        better = Z[l] < best
+        best = np.where(better, Z[l], best)
+        lab = np.where(better, l, lab)
+    return lab
+
+
+def aggregate_wta(I, V, lam, r, d, mode=MODE_HGF, method="solve", return_z=False):
+    """Multi-label aggregation (filter every slice of V(x, y, l)) followed by WTA."""
+    Z = hgf_filter(I, V, lam, r, d, mode=mode, method=method)
+    lab = wta(Z)
+    if return_z:
+        return lab, Z
+    return lab
+
+
+def _orderable_u32(f32: np.ndarray) -> np.ndarray:
+    """Monotone map of float32 bit patterns to uint32 (negative: ~bits; non-negative: bits | 2^31)."""
+    f = np.asarray(f32, dtype=np.float32) + np.float32(0.0)     # -0.0 -> +0.0
+    b = f.view(np.uint32).astype(np.uint64)
+    neg = (b >> np.uint64(31)) & np.uint64(1)
+    return np.where(neg == 1, (~b) & np.uint64(0xFFFFFFFF), b | np.uint64(0x80000000)).astype(np.uint64)
+
+
+def pack_keys(cost_f32: np.ndarray, labels: np.ndarray) -> np.ndarray:
+    """key = orderable(cost) << 32 | label  (uint64): min over keys = (min cost, lowest label)."""
+    return (_orderable_u32(cost_f32) << np.uint64(32)) | np.asarray(labels).astype(np.uint64)
+
+
+def unpack_keys(keys: np.ndarray):
+    """Inverse of pack_keys: returns (cost float32, label int32)."""
+    keys = np.asarray(keys, dtype=np.uint64)
+    o = (keys >> np.uint64(32)) & np.uint64(0xFFFFFFFF)
+    hi = (o >> np.uint64(31)) & np.uint64(1)
+    b = np.where(hi == 1, o & np.uint64(0x7FFFFFFF), (~o) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    return b.view(np.float32), (keys & np.uint64(0xFFFFFFFF)).astype(np.int32)

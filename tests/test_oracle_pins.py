@@ -1,0 +1,299 @@
+"""Pins for oracle/ against things other than itself (-m "not gpu").
+
+Each test names the passage it follows.  Pins: brute force, exact integer arithmetic,
+independent solvers (LU inverse / least squares / Cramer), closed forms, He et al.'s
+textbook closed form, invariants, and SPEC/closed-form fixtures in tests/golden/.
+Several tests also show that the plausible *misreadings* of the paper (printed
+alpha^0_00, Eq11 without gamma, dropped intercept penalty) FAIL the same pins.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+RNG = np.random.default_rng(12345)
+
+
+# ---------------------------------------------------------------- box filter (Prop 2)
+@pytest.mark.parametrize("shape,r", [((9, 11), 1), ((9, 11), 2), ((5, 3), 3), ((1, 1), 2), ((7, 13), 7), ((16, 4), 1)])
+def test_box_sum_exact_on_integers(shape, r):
+    X = RNG.integers(0, 2 ** 20, size=shape).astype(np.float64)
+    assert np.array_equal(O.box_sum(X, r), O.box_sum_brute(X, r))
+
+
+def test_box_sum_golden():
+    g = GOLD["box_sum_2x2_r1"]
+    assert np.array_equal(O.box_sum(np.array(g["plane"], float), g["r"]), np.array(g["expect"], float))
+    g = GOLD["box_sum_ones_2x2_r1"]
+    assert np.array_equal(O.box_sum(np.array(g["plane"], float), g["r"]), np.array(g["expect"], float))
+    g = GOLD["box_sum_ones_5x5_r1"]
+    B = O.box_sum(np.ones((g["H"], g["W"])), g["r"])
+    assert B[0, 0] == g["corner"] and B[2, 2] == g["centre"]
+    assert np.array_equal(O.box_count(g["H"], g["W"], g["r"]), B)
+    g = GOLD["box_mean_half"]
+    assert np.allclose(O.box_mean(np.array(g["plane"], float), g["r"]), g["expect"], rtol=0, atol=1e-15)
+
+
+def test_box_linearity_and_count():
+    X, Y = RNG.random((2, 12, 17))
+    a, b = 0.3, -2.5
+    assert np.allclose(O.box_sum(a * X + b * Y, 3), a * O.box_sum(X, 3) + b * O.box_sum(Y, 3), atol=1e-12)
+    for H, W, r in [(1, 1, 3), (4, 9, 2), (20, 20, 9)]:
+        assert np.array_equal(O.box_count(H, W, r), O.box_sum_brute(np.ones((H, W)), r))
+
+
+# ---------------------------------------------------------------- polynomial guidance
+def test_poly_guidance_golden_and_order():
+    g = GOLD["poly_half_d3"]
+    G = O.poly_guidance(np.full((1, 2, 2), g["value"]), g["d"])
+    assert np.array_equal(G[:, 0, 0], np.array(g["expect"]))
+    I = RNG.random((3, 4, 5))
+    G = O.poly_guidance(I, 2)
+    expect = np.stack([I[0], I[0] ** 2, I[1], I[1] ** 2, I[2], I[2] ** 2])   # channel-major
+    assert np.allclose(G, expect, rtol=1e-15, atol=0)
+    assert np.array_equal(O.poly_guidance(I, 1), I)
+
+
+# ---------------------------------------------------------------- Gram (Prop 2, Eq12)
+def test_gram_golden():
+    g = GOLD["gram_2x2_r1"]
+    Gram, _ = O.gram_planes(np.array([g["plane"]], float), g["r"])
+    assert np.all(Gram[1, 1] == g["expect_G11"])
+    assert np.all(Gram[0, 1] == g["expect_G01"]) and np.all(Gram[0, 0] == g["expect_G00"])
+
+
+def test_gram_vs_naive_window_dot_products():
+    H, W, r, n = 7, 9, 2, 3
+    G = RNG.integers(0, 1000, size=(n, H, W)).astype(np.float64)
+    Y = RNG.integers(0, 1000, size=(H, W)).astype(np.float64)
+    Gram, Gy = O.gram_planes(G, r, Y)
+    ext = np.concatenate([np.ones((1, H, W)), G])
+    for y in range(H):
+        for x in range(W):
+            sl = (slice(None), slice(max(0, y - r), y + r + 1), slice(max(0, x - r), x + r + 1))
+            C = ext[sl].reshape(n + 1, -1)
+            assert np.array_equal(Gram[:, :, y, x], C @ C.T)
+            assert np.array_equal(Gy[:, y, x], C @ Y[sl[1:]].ravel())
+
+
+# ---------------------------------------------------------------- Prop 1 (Eq4)
+def _random_windows(N, K, rng):
+    C = rng.random((N, K))
+    C[:, 0] = 1.0                       # c_0 = ones
+    return C
+
+
+@pytest.mark.parametrize("N", [9, 25, 225])
+@pytest.mark.parametrize("K", [1, 2, 4, 7, 10])
+@pytest.mark.parametrize("lam", [0.05, 1.0, 2.0])
+def test_alpha_inverse_identity(N, K, lam):
+    """(lam E + sum c_i c_i^T)(lam^-1 E + sum alpha_ij c_i c_j^T) = E in the |Omega|-dim space (Prop 1)."""
+    rng = np.random.default_rng(N * 100 + K)
+    C = _random_windows(N, K, rng)
+    alpha = O.alpha_recursion(C.T @ C, lam)
+    A = lam * np.eye(N) + C @ C.T
+    Ainv = np.eye(N) / lam + C @ alpha @ C.T
+    assert np.linalg.norm(A @ Ainv - np.eye(N)) <= 1e-8
+    # M^-1 = -lam alpha where M = lam E + Gram (Woodbury), vs an LU inverse (np.linalg.inv)
+    Minv = np.linalg.inv(lam * np.eye(K) + C.T @ C)
+    assert np.abs(-lam * alpha - Minv).max() <= 1e-9 * np.abs(Minv).max()
+    assert np.abs(alpha - alpha.T).max() <= 1e-9 * np.abs(alpha).max()
+
+
+def test_alpha_golden_and_misreadings_fail():
+    for key in ("alpha00_lambda1", "alpha00_lambda2"):
+        g = GOLD[key]
+        a = O.alpha_recursion(np.array([[g["G00"]]]), g["lambda"])
+        assert a[0, 0] == pytest.approx(g["expect"], rel=1e-15)
+    # printed init -(lambda+G00)^-1 fails the identity at lambda = 2 (reading F1)
+    g = GOLD["alpha00_lambda2"]
+    assert -1.0 / (g["lambda"] + g["G00"]) == pytest.approx(g["printed_formula_value"])
+    N, K, lam = 25, 4, 0.05
+    C = _random_windows(N, K, np.random.default_rng(7))
+    Gram = C.T @ C
+
+    def recursion(init_printed=False, drop_gamma=False):
+        inv = 1 / lam
+        al = np.zeros((K, K))
+        al[0, 0] = -1 / (lam + Gram[0, 0]) if init_printed else -inv / (lam + Gram[0, 0])
+        for k in range(1, K):
+            u = al[:k, :k] @ Gram[:k, k]
+            gam = -1 / (1 + inv * Gram[k, k] + Gram[k, :k] @ u)
+            al[:k, :k] = (1.0 if drop_gamma else gam) * np.outer(u, u) + al[:k, :k]
+            al[:k, k] = al[k, :k] = inv * gam * u
+            al[k, k] = inv * inv * gam
+        return al
+
+    def resid(al):
+        return np.linalg.norm((lam * np.eye(N) + C @ C.T) @ (np.eye(N) / lam + C @ al @ C.T) - np.eye(N))
+
+    assert resid(recursion()) < 1e-9
+    assert np.allclose(recursion(), O.alpha_recursion(Gram, lam), rtol=1e-12, atol=0)
+    assert resid(recursion(init_printed=True)) > 1.0          # F1 misreading fails
+    assert resid(recursion(drop_gamma=True)) > 1.0            # F2 misreading fails
+
+
+def test_gamma_denominator_at_least_one():
+    C = _random_windows(49, 8, np.random.default_rng(3))
+    Gram = C.T @ C
+    lam = 0.05
+    al = O.alpha_recursion(Gram, lam)
+    # -1/gamma_kappa = 1 + c^T A^-1 c >= 1 ; alpha_kk = lam^-2 gamma  => gamma in [-1, 0)
+    gam = np.diag(al)[1:] * lam * lam
+    assert np.all(gam < 0) and np.all(gam >= -1)
+
+
+# ---------------------------------------------------------------- weights (Eq2, Eq5/Eq13)
+def test_weights_closed_forms():
+    g = GOLD["weights_n0"]
+    # n = 0: only c_0 = ones, Y = 1 in a 3x3 window (one pixel at the centre of a 3x3 image, r = 1)
+    Gram = np.array([[g["N"]]], float)
+    Gy = np.array([g["N"] * g["Y"]])
+    al = O.alpha_recursion(Gram, g["lambda"])
+    W = O.weights_eq13(al, Gram, Gy, g["lambda"])
+    assert W[0] == pytest.approx(g["expect"], rel=1e-14)
+
+
+@pytest.mark.parametrize("mode", ["hgf", "gf"])
+def test_weights_three_solvers_agree(mode):
+    """Prop-1 + Eq13 == dense solve == augmented least squares [X; sqrt(lam) D] w = [y; 0] (Eq7 / Eq15)."""
+    H, W, r, lam = 6, 7, 2, 0.05
+    I = RNG.random((2, H, W))
+    Y = RNG.random((H, W))
+    G = O.poly_guidance(I, 2)
+    w_solve = O.hgf_weights(G, Y, lam, r, mode=mode, method="solve")
+    w_paper = O.hgf_weights(G, Y, lam, r, mode=mode, method="paper")
+    n = G.shape[0]
+    D = np.eye(n + 1) if mode == "hgf" else np.diag([0.0] + [1.0] * n)
+    for y in range(H):
+        for x in range(W):
+            sl = (slice(max(0, y - r), y + r + 1), slice(max(0, x - r), x + r + 1))
+            X = np.stack([np.ones(Y[sl].size)] + [G[i][sl].ravel() for i in range(n)], 1)
+            A = np.vstack([X, np.sqrt(lam) * D])
+            rhs = np.concatenate([Y[sl].ravel(), np.zeros(n + 1)])
+            w_ls = np.linalg.lstsq(A, rhs, rcond=None)[0]
+            assert np.allclose(w_solve[:, y, x], w_ls, rtol=1e-9, atol=1e-9)
+    assert np.allclose(w_paper, w_solve, rtol=1e-7, atol=1e-7)
+
+
+def test_hgf_n1_cramer():
+    """n = 1 (gray, d = 1): 2x2 system [[lam+N, S1],[S1, lam+S11]] w = [Sy, S1y] by Cramer's rule."""
+    H, W, r, lam = 8, 9, 2, 0.05
+    I = RNG.random((1, H, W))
+    Y = RNG.random((H, W))
+    N = O.box_count(H, W, r)
+    S1 = O.box_sum(I[0], r)
+    S11 = O.box_sum(I[0] * I[0], r)
+    Sy = O.box_sum(Y, r)
+    S1y = O.box_sum(I[0] * Y, r)
+    a, b, c, d = lam + N, S1, S1, lam + S11
+    det = a * d - b * c
+    w0 = (Sy * d - b * S1y) / det
+    w1 = (a * S1y - c * Sy) / det
+    w = O.hgf_weights(I, Y, lam, r, mode="hgf")
+    assert np.allclose(w[0], w0, rtol=1e-10) and np.allclose(w[1], w1, rtol=1e-10)
+    Z = (O.box_sum(w0, r) + I[0] * O.box_sum(w1, r)) / N          # Eq14 written out
+    assert np.allclose(O.hgf_filter(I, Y, lam, r, 1), Z, rtol=1e-10, atol=1e-12)
+
+
+# ---------------------------------------------------------------- whole filter (Eq8/Eq14)
+@pytest.mark.parametrize("mode", ["hgf", "gf"])
+@pytest.mark.parametrize("m,d,r,H,W", [(3, 2, 2, 9, 11), (1, 3, 1, 6, 5), (2, 1, 3, 7, 7), (3, 3, 2, 5, 13)])
+def test_filter_definition_vs_brute_vs_paper(mode, m, d, r, H, W):
+    rng = np.random.default_rng(m * 31 + d * 7 + r)
+    I = rng.random((m, H, W))
+    Y = rng.random((H, W))
+    lam = 0.05
+    z_def = O.hgf_filter(I, Y, lam, r, d, mode=mode)
+    z_brute = O.hgf_filter_brute(I, Y, lam, r, d, mode=mode)
+    z_paper = O.hgf_filter(I, Y, lam, r, d, mode=mode, method="paper")
+    assert np.allclose(z_def, z_brute, rtol=1e-9, atol=1e-10)
+    assert np.allclose(z_paper, z_def, rtol=1e-6, atol=1e-8)
+
+
+def test_intercept_penalty_distinguishes_modes():
+    """HGF (Eq7) penalises w(0); GF (Eq15) does not — a dropped/added intercept term changes Z."""
+    I = RNG.random((3, 10, 10))
+    Y = RNG.random((10, 10))
+    zh = O.hgf_filter(I, Y, 0.05, 2, 1, mode="hgf")
+    zg = O.hgf_filter(I, Y, 0.05, 2, 1, mode="gf")
+    assert np.abs(zh - zg).max() > 1e-4
+
+
+@pytest.mark.parametrize("m", [1, 3])
+def test_gf_mode_equals_he_closed_form(m):
+    """GF mode (§5.1) == He et al.'s closed form with eps_p = lambda / N_p (B is a sum, F7)."""
+    H, W, r, lam = 12, 15, 3, 0.05
+    I = RNG.random((m, H, W))
+    Y = RNG.random((H, W))
+    eps = lam / O.box_count(H, W, r)
+    assert np.allclose(O.hgf_filter(I, Y, lam, r, 1, mode="gf"), O.gf_he(I, Y, eps, r), rtol=1e-10, atol=1e-12)
+
+
+# ---------------------------------------------------------------- invariants (north-star oracle checks)
+def test_gf_constant_in_constant_out_and_large_eps_box_mean():
+    I = RNG.random((3, 11, 13))
+    c = 0.37
+    z = O.hgf_filter(I, np.full((11, 13), c), 0.05, 2, 2, mode="gf")
+    assert np.abs(z - c).max() <= 1e-12
+    Y = RNG.random((11, 13))
+    z = O.hgf_filter(I, Y, 1e9, 2, 2, mode="gf")               # slopes -> 0, Z -> A(A(Y))
+    assert np.abs(z - O.box_mean(O.box_mean(Y, 2), 2)).max() <= 1e-7
+
+
+def test_hgf_linearity_and_large_lambda_limit():
+    I = RNG.random((3, 9, 10))
+    Y1, Y2 = RNG.random((2, 9, 10))
+    f = lambda Y, lam=0.05: O.hgf_filter(I, Y, lam, 2, 2)
+    assert np.allclose(f(2 * Y1 - 3 * Y2), 2 * f(Y1) - 3 * f(Y2), atol=1e-11)
+    lam = 1e9
+    G = O.poly_guidance(I, 2)
+    ext = np.concatenate([np.ones((1, 9, 10)), G])
+    limit = sum(ext[k] * O.box_mean(O.box_sum(ext[k] * Y1, 2), 2) for k in range(ext.shape[0]))
+    assert np.abs(lam * f(Y1, lam) - limit).max() <= 1e-6 * np.abs(limit).max()
+
+
+def test_wta_golden_and_brute():
+    g = GOLD["wta_ties"]
+    Z = np.array(g["costs"])[:, None, :]                        # (L, 1, 2)
+    assert O.wta(Z)[0].tolist() == g["expect"]
+    Z = RNG.integers(0, 4, size=(6, 5, 7)).astype(np.float64)    # many exact ties
+    lab = O.wta(Z)
+    for y in range(5):
+        for x in range(7):
+            col = list(Z[:, y, x])
+            assert lab[y, x] == col.index(min(col))
+
+
+def test_label_permutation_and_affine_invariance():
+    I = RNG.random((3, 10, 12))
+    V = RNG.random((7, 10, 12))
+    lab, Z = O.aggregate_wta(I, V, 0.05, 2, 2, return_z=True)
+    srt = np.sort(Z, axis=0)
+    clear = (srt[1] - srt[0]) > 1e-9
+    perm = RNG.permutation(7)
+    lab_p = O.aggregate_wta(I, V[perm], 0.05, 2, 2)
+    assert np.array_equal(perm[lab_p][clear], lab[clear])          # argmin(V o perm) = perm^-1(argmin V)
+    lab_a = O.aggregate_wta(I, 3.0 * V + 0.25, 0.05, 2, 2)
+    assert np.array_equal(lab_a[clear], lab[clear])
+
+
+def test_keys_order_and_roundtrip():
+    cost = np.array([0.5, -0.0, 0.0, -1.5, 2.0, np.float32(1e-30), -np.float32(1e-30)], np.float32)
+    lab = np.array([3, 7, 1, 2, 9, 4, 5], np.int32)
+    k = O.pack_keys(cost, lab)
+    c2, l2 = O.unpack_keys(k)
+    assert np.array_equal(l2, lab)
+    assert np.array_equal(c2, cost + np.float32(0.0))
+    order = np.argsort(k, kind="stable")
+    lex = sorted(range(len(cost)), key=lambda i: (float(cost[i]), int(lab[i])))
+    assert order.tolist() == lex
+    # min over per-shard keys == global (min cost, lowest label)
+    V = RNG.integers(0, 5, size=(8, 6)).astype(np.float32)   # (L, P) with ties
+    full = O.pack_keys(V.min(0), V.argmin(0))
+    shards = [O.pack_keys(V[a:b].min(0), a + V[a:b].argmin(0)) for a, b in [(0, 3), (3, 5), (5, 8)]]
+    assert np.array_equal(np.minimum.reduce(shards), full)
