@@ -1,0 +1,139 @@
+/*
+ * hgf.h — C ABI of the B200-native Hardware-Efficient Guided Filter (HGF) hot path.
+ *
+ * Paper: Dai et al., "Hardware-Efficient Guided Image Filtering for Multi-Label Problem",
+ * CVPR 2018, arXiv 1803.00005.  "P:n" = line n of the paper's LaTeX source.
+ *
+ * The path (BASELINE.json north_star):
+ *   1. polynomial guidance  G_{(i-1)d+j} = I_i^j               (§4.2; P:630 uses d = 2)
+ *   2. label-independent statistics: Gram planes G_ij = B(G_i G_j) (Prop 2; Eq12)
+ *      and the regularised inverse by the paper's recursion (Prop 1 / Eq4; Eq11),
+ *      computed ONCE per frame in float64
+ *   3. per cost slice (label) l: box sums of p and G_k p, coefficients w (Eq13, reassociated),
+ *      box sums of w, output Z (Eq14 P:328-333 == Eq8)
+ *   4. winner-takes-all argmin over labels, ties -> lowest label
+ *
+ * Conventions for every entry point below
+ *   - B(.) is a box SUM over the (2r+1)x(2r+1) window clipped to the image; eps is the
+ *     paper's lambda against those sums (Eq7).  N_p = clipped window pixel count.
+ *   - All image arrays are dense, row-major float32 planes; a stack of planes is plane-major:
+ *       guide        [n_guide][H][W]   raw guidance I, values expected in [0, 1]
+ *       cost_volume  [L][H][W]         slice l is label (label_offset + l)
+ *       labels_out   [H][W] int32      argmin label
+ *   - Pointers passed to hgf_filter / hgf_aggregate_wta* / hgf_unpack_keys are CUDA DEVICE
+ *     pointers owned by the caller.  These calls allocate nothing, copy nothing host<->device and
+ *     are asynchronous on the handle's stream: results are valid after that stream synchronises.
+ *     (hgf_aggregate_wta_host is the one entry point that takes host pointers; see there.)
+ *   - The library owns only its scratch (guidance planes, statistics planes, coefficient buffer),
+ *     allocated by hgf_create* and freed by hgf_destroy.
+ *   - A handle is bound to the CUDA device current at create time and is not thread-safe:
+ *     use one handle per host thread / stream.
+ *   - Errors: every call returns an hgf_status; HGF_ERR_CUDA reports a CUDA failure (including
+ *     an asynchronous fault from earlier work on the stream); hgf_last_error() gives detail.
+ *     No call falls back to a CPU implementation.
+ */
+#ifndef HGF_H_
+#define HGF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HGF_API __attribute__((visibility("default")))
+#else
+#define HGF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hgf_ctx* hgf_handle;
+
+typedef enum {
+  HGF_OK = 0,
+  HGF_ERR_INVALID_ARGUMENT = 1, /* bad size, null pointer, eps <= 0 or non-finite, ...          */
+  HGF_ERR_UNSUPPORTED = 2,      /* n = n_guide*poly_degree > HGF_MAX_CHANNELS, radius > HGF_MAX_RADIUS */
+  HGF_ERR_OUT_OF_MEMORY = 3,    /* scratch allocation failed                                    */
+  HGF_ERR_CUDA = 4              /* a CUDA runtime error (launch failure or asynchronous fault)  */
+} hgf_status;
+
+/* Regression modes.
+ * HGF_MODE_HGF: the paper's HGF, Eq7: lambda ||w||^2 penalises ALL n+1 coefficients,
+ *               including the intercept w(0).
+ * HGF_MODE_GF : the paper's §5.1 guided filter, Eq15/16: slopes penalised, intercept
+ *               free (He et al.'s GF with eps_p = lambda / N_p). */
+enum { HGF_MODE_HGF = 0, HGF_MODE_GF = 1 };
+
+#define HGF_MAX_CHANNELS 20 /* n = n_guide * poly_degree  (BASELINE config 5 sweeps n = 1..20) */
+#define HGF_MAX_RADIUS 32
+
+/* Create a handle for W x H images with an n_guide-channel raw guide, polynomial degree
+ * poly_degree (n = n_guide * poly_degree synthesised channels, §4.2), window radius `radius`
+ * (side 2r+1) and regulariser eps = lambda > 0 (P:151 needs lambda^-1).  HGF mode, legacy
+ * default stream.  Allocates the per-frame scratch on the current device.
+ * Errors: INVALID_ARGUMENT (W,H,n_guide,poly_degree,radius < 1, eps <= 0 or non-finite, out==NULL),
+ *         UNSUPPORTED (n > HGF_MAX_CHANNELS or radius > HGF_MAX_RADIUS), OUT_OF_MEMORY, CUDA. */
+HGF_API hgf_status hgf_create(hgf_handle* out, int W, int H, int n_guide, int poly_degree, int radius, double eps);
+
+/* As hgf_create, with mode (HGF_MODE_HGF | HGF_MODE_GF) and a cudaStream_t (NULL = legacy default). */
+HGF_API hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_degree, int radius,
+                         double eps, int mode, void* cuda_stream);
+
+/* Free the handle and its scratch (synchronises the handle's stream first).  NULL is accepted. */
+HGF_API hgf_status hgf_destroy(hgf_handle h);
+
+/* Re-bind the handle to another cudaStream_t (NULL = legacy default stream). */
+HGF_API hgf_status hgf_set_stream(hgf_handle h, void* cuda_stream);
+
+/* Filter one slice (Fig 2 flowchart): dst = HGF(src; guide).
+ * guide [n_guide][H][W], src [H][W], dst [H][W] (device, float32; dst must not alias guide/src).
+ * Runs steps 1-3 of the path with L = 1. */
+HGF_API hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float* dst);
+
+/* Multi-label aggregation + WTA: filter every slice of cost_volume [L][H][W] with the
+ * guidance synthesised from guide, write labels_out[p] = argmin_l Z_l(p) (ties -> lowest l).
+ * L >= 1.  Equivalent to hgf_aggregate_wta_ex(h, guide, cost_volume, L, 0, labels_out, NULL, NULL, NULL). */
+HGF_API hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L,
+                             int32_t* labels_out);
+
+/* Extended form for label shards and debugging.  Label index reported = label_offset + l.
+ * Outputs (each may be NULL; at least one must be non-NULL):
+ *   labels_out    int32  [H][W]     argmin label
+ *   min_cost_out  float  [H][W]     min_l Z_l
+ *   filtered_out  float  [L][H][W]  every filtered slice Z_l (same arithmetic as the WTA path)
+ *   keys_out      int64  [H][W]     packed key = (orderable(min cost) << 32 | label) XOR 2^63, where
+ *                 orderable(f) = bits(f) | 2^31 for f >= +0 (-0.0 is canonicalised to +0.0),
+ *                 ~bits(f) for f < 0.  The unsigned key orders (cost, label) lexicographically;
+ *                 the XOR with 2^63 makes the SIGNED int64 order identical, so the label-sharded
+ *                 merge is an int64 allreduce-MIN (NCCL ncclInt64/ncclMin, or gloo) over shards.
+ * label_offset >= 0 and label_offset + L <= 2^31 - 1. */
+HGF_API hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* cost_volume, int L,
+                                int label_offset, int32_t* labels_out, float* min_cost_out,
+                                float* filtered_out, int64_t* keys_out);
+
+/* Unpack merged (signed) keys [H][W] into labels_out (int32, may be NULL) and min_cost_out (float, may be NULL). */
+HGF_API hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_out, float* min_cost_out);
+
+/* End-to-end form with HOST buffers: guide_host [n_guide][H][W], cost_host [L][H][W] (float32,
+ * preferably pinned), labels_host [H][W] int32.  Copies the inputs host->device in label chunks on
+ * the handle's stream, overlapped with the aggregation of the previous chunk, then copies the labels
+ * back and synchronises the stream before returning.  Device staging buffers are owned by the handle
+ * (allocated on first use, sized by the chunk).  Errors as hgf_aggregate_wta_ex. */
+HGF_API hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const float* cost_host, int L,
+                                  int32_t* labels_host);
+
+/* Number of kernel launches the last hgf_filter / hgf_aggregate_wta* call enqueued. */
+HGF_API int hgf_last_launch_count(hgf_handle h);
+
+/* Static description of a status code. */
+HGF_API const char* hgf_status_string(hgf_status s);
+
+/* Detail for the last failure on this handle ("" if none).  Valid until the next call on h. */
+HGF_API const char* hgf_last_error(hgf_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HGF_H_ */

@@ -1,0 +1,220 @@
+"""B200-native Hardware-Efficient Guided Filter (HGF) hot path: Python binding of libhgf.so.
+
+Thin ctypes marshalling over the C ABI in ``include/hgf.h`` (same names).  PyTorch supplies
+device memory, streams and process groups; every step of the path runs in the library's
+CUDA kernels.  There is no CPU fallback: if the shared library is missing or no CUDA device is
+present, constructing :class:`HGF` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["HGF", "HGFError", "lib", "lib_path", "MODE_HGF", "MODE_GF", "EXPORTED_SYMBOLS",
+           "merge_keys_allreduce", "shard_range"]
+
+MODE_HGF = 0
+MODE_GF = 1
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libhgf.so")
+
+# Every entry point declared in include/hgf.h (tests check the .so exports all of them).
+EXPORTED_SYMBOLS = (
+    "hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter",
+    "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
+    "hgf_last_launch_count", "hgf_status_string", "hgf_last_error",
+)
+
+_lib = None
+
+
+class HGFError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libhgf.so (built by ``make`` / ``__graft_entry__.build()``); raise if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise ImportError(f"{lib_path} not built: run `make -j8` (or __graft_entry__.build()); no CPU fallback")
+    L = ctypes.CDLL(lib_path)
+    c_int, c_double, vp = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+    L.hgf_create.argtypes = [ctypes.POINTER(vp), c_int, c_int, c_int, c_int, c_int, c_double]
+    L.hgf_create_ex.argtypes = [ctypes.POINTER(vp), c_int, c_int, c_int, c_int, c_int, c_double, c_int, vp]
+    L.hgf_destroy.argtypes = [vp]
+    L.hgf_set_stream.argtypes = [vp, vp]
+    L.hgf_filter.argtypes = [vp, vp, vp, vp]
+    L.hgf_aggregate_wta.argtypes = [vp, vp, vp, c_int, vp]
+    L.hgf_aggregate_wta_ex.argtypes = [vp, vp, vp, c_int, c_int, vp, vp, vp, vp]
+    L.hgf_unpack_keys.argtypes = [vp, vp, vp, vp]
+    L.hgf_aggregate_wta_host.argtypes = [vp, vp, vp, c_int, vp]
+    L.hgf_last_launch_count.argtypes = [vp]
+    L.hgf_last_launch_count.restype = c_int
+    L.hgf_status_string.argtypes = [c_int]
+    L.hgf_status_string.restype = ctypes.c_char_p
+    L.hgf_last_error.argtypes = [vp]
+    L.hgf_last_error.restype = ctypes.c_char_p
+    for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
+                 "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host"):
+        getattr(L, name).restype = c_int
+    _lib = L
+    return L
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class HGF:
+    """Handle over ``hgf_create_ex``: W x H images, raw guide with ``n_guide`` channels, polynomial
+    degree ``poly_degree`` (n = n_guide * poly_degree, §4.2), radius r, eps = lambda,
+    mode ``"hgf"`` (Eq7) or ``"gf"`` (§5.1 Eq15/16)."""
+
+    def __init__(self, W, H, n_guide, poly_degree, radius, eps, mode="hgf", device=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise HGFError("HGF needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.W, self.H, self.m, self.d, self.r, self.eps = W, H, n_guide, poly_degree, radius, eps
+        self.n = n_guide * poly_degree
+        self.mode = {"hgf": MODE_HGF, "gf": MODE_GF}[mode] if isinstance(mode, str) else int(mode)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            st = lib().hgf_create_ex(ctypes.byref(h), W, H, n_guide, poly_degree, radius, float(eps), self.mode,
+                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if st != 0:
+            raise HGFError(f"hgf_create_ex: {lib().hgf_status_string(st).decode()}")
+        self._h = h
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st, what):
+        if st != 0:
+            raise HGFError(f"{what}: {lib().hgf_status_string(st).decode()}: {lib().hgf_last_error(self._h).decode()}")
+
+    def _bind_stream(self):
+        s = self._torch.cuda.current_stream(self.device).cuda_stream
+        self._check(lib().hgf_set_stream(self._h, ctypes.c_void_p(s)), "hgf_set_stream")
+
+    def _dev(self, t, shape, dtype, name):
+        torch = self._torch
+        if not isinstance(t, torch.Tensor) or t.device != self.device or t.dtype != dtype or not t.is_contiguous():
+            raise HGFError(f"{name} must be a contiguous {dtype} tensor on {self.device}")
+        if tuple(t.shape) != tuple(shape):
+            raise HGFError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        return t
+
+    @property
+    def last_launch_count(self):
+        return lib().hgf_last_launch_count(self._h)
+
+    # ------------------------------------------------------------------ API (names as in hgf.h)
+    def filter(self, guide, src, dst=None):
+        torch = self._torch
+        self._dev(guide, (self.m, self.H, self.W), torch.float32, "guide")
+        self._dev(src, (self.H, self.W), torch.float32, "src")
+        if dst is None:
+            dst = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+        self._dev(dst, (self.H, self.W), torch.float32, "dst")
+        self._bind_stream()
+        self._check(lib().hgf_filter(self._h, _ptr(guide), _ptr(src), _ptr(dst)), "hgf_filter")
+        return dst
+
+    def aggregate_wta(self, guide, cost_volume, labels_out=None):
+        torch = self._torch
+        L = cost_volume.shape[0]
+        self._dev(guide, (self.m, self.H, self.W), torch.float32, "guide")
+        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
+        if labels_out is None:
+            labels_out = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
+        self._dev(labels_out, (self.H, self.W), torch.int32, "labels_out")
+        self._bind_stream()
+        self._check(lib().hgf_aggregate_wta(self._h, _ptr(guide), _ptr(cost_volume), L, _ptr(labels_out)),
+                    "hgf_aggregate_wta")
+        return labels_out
+
+    def aggregate_wta_ex(self, guide, cost_volume, label_offset=0, labels=True, min_cost=False, filtered=False,
+                         keys=False, out=None):
+        """Returns a dict with the requested outputs ('labels', 'min_cost', 'filtered', 'keys')."""
+        torch = self._torch
+        L = cost_volume.shape[0]
+        self._dev(guide, (self.m, self.H, self.W), torch.float32, "guide")
+        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
+        out = dict(out or {})
+        dev, HW = self.device, (self.H, self.W)
+        if labels and "labels" not in out:
+            out["labels"] = torch.empty(HW, dtype=torch.int32, device=dev)
+        if min_cost and "min_cost" not in out:
+            out["min_cost"] = torch.empty(HW, dtype=torch.float32, device=dev)
+        if filtered and "filtered" not in out:
+            out["filtered"] = torch.empty((L,) + HW, dtype=torch.float32, device=dev)
+        if keys and "keys" not in out:
+            out["keys"] = torch.empty(HW, dtype=torch.int64, device=dev)
+        if "labels" in out:
+            self._dev(out["labels"], HW, torch.int32, "labels")
+        if "min_cost" in out:
+            self._dev(out["min_cost"], HW, torch.float32, "min_cost")
+        if "filtered" in out:
+            self._dev(out["filtered"], (L,) + HW, torch.float32, "filtered")
+        if "keys" in out:
+            self._dev(out["keys"], HW, torch.int64, "keys")
+        self._bind_stream()
+        self._check(lib().hgf_aggregate_wta_ex(self._h, _ptr(guide), _ptr(cost_volume), L, int(label_offset),
+                                               _ptr(out.get("labels")), _ptr(out.get("min_cost")),
+                                               _ptr(out.get("filtered")), _ptr(out.get("keys"))),
+                    "hgf_aggregate_wta_ex")
+        return out
+
+    def unpack_keys(self, keys, labels_out=None, min_cost_out=None):
+        torch = self._torch
+        HW = (self.H, self.W)
+        self._dev(keys, HW, torch.int64, "keys")
+        if labels_out is None:
+            labels_out = torch.empty(HW, dtype=torch.int32, device=self.device)
+        if min_cost_out is None:
+            min_cost_out = torch.empty(HW, dtype=torch.float32, device=self.device)
+        self._bind_stream()
+        self._check(lib().hgf_unpack_keys(self._h, _ptr(keys), _ptr(labels_out), _ptr(min_cost_out)),
+                    "hgf_unpack_keys")
+        return labels_out, min_cost_out
+
+    def aggregate_wta_host(self, guide_host, cost_host, labels_host=None):
+        """Host tensors (CPU float32; pinned for overlap) in, host int32 labels out; synchronous."""
+        torch = self._torch
+        L = cost_host.shape[0]
+        for t, nm in ((guide_host, "guide_host"), (cost_host, "cost_host")):
+            if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous():
+                raise HGFError(f"{nm} must be a contiguous float32 CPU tensor")
+        if labels_host is None:
+            labels_host = torch.empty((self.H, self.W), dtype=torch.int32, pin_memory=True)
+        self._bind_stream()
+        self._check(lib().hgf_aggregate_wta_host(self._h, _ptr(guide_host), _ptr(cost_host), L, _ptr(labels_host)),
+                    "hgf_aggregate_wta_host")
+        return labels_host
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().hgf_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_range(L, world, rank):
+    """Contiguous label range [l0, l1) of `rank` (first L mod world ranks get one extra label)."""
+    base, extra = divmod(L, world)
+    l0 = rank * base + min(rank, extra)
+    return l0, l0 + base + (1 if rank < extra else 0)
+
+
+def merge_keys_allreduce(keys, group=None):
+    """Label-sharded WTA merge: in-place int64 allreduce-MIN of the signed packed keys (hgf.h)."""
+    import torch.distributed as dist
+    dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+    return keys

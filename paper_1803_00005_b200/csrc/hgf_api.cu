@@ -1,0 +1,311 @@
+// C ABI of the HGF hot path (declared in include/hgf.h).  Validation, scratch ownership, stream
+// handling and launch sequencing; every step of the path runs in the kernels of hgf_kernels.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "../../include/hgf.h"
+#include "hgf_common.cuh"
+#include "hgf_launch.h"
+
+struct hgf_ctx {
+  int W = 0, H = 0, m = 0, d = 0, n = 0, r = 0, mode = 0;
+  double eps = 0.0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  float* G = nullptr;          // [n][H][W]     polynomial guidance (K1)
+  float* stats = nullptr;      // [NS][H][W]    P' upper triangle + nu (K3)
+  float* wbuf = nullptr;       // [lcap][n+1][H][W] per-slice coefficients w (K4a -> K4b)
+  int lcap = 0;                // labels per coefficient chunk
+  float* best_cost = nullptr;  // [H][W] running WTA state across chunks
+  int32_t* best_label = nullptr;
+  // host-buffer path staging (lazily allocated)
+  float* st_guide = nullptr;
+  float* st_vol[2] = {nullptr, nullptr};
+  int32_t* st_labels = nullptr;
+  int st_chunk = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_used[2] = {nullptr, nullptr};
+  int launches = 0;
+  std::string err;
+};
+
+namespace {
+
+hgf_status fail(hgf_ctx* h, hgf_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+hgf_status cuda_fail(hgf_ctx* h, cudaError_t e, const char* where) {
+  return fail(h, HGF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define HGF_CK(h, expr)                                   \
+  do {                                                    \
+    cudaError_t e_ = (expr);                              \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #expr); \
+    (h)->launches++;                                      \
+  } while (0)
+
+size_t coef_budget_bytes() {
+  const char* s = std::getenv("HGF_COEF_BUDGET_MB");
+  long long mb = s ? std::atoll(s) : 2048;
+  if (mb < 1) mb = 1;
+  return (size_t)mb << 20;
+}
+
+void release(hgf_ctx* h) {
+  cudaFree(h->G);
+  cudaFree(h->stats);
+  cudaFree(h->wbuf);
+  cudaFree(h->best_cost);
+  cudaFree(h->best_label);
+  cudaFree(h->st_guide);
+  cudaFree(h->st_vol[0]);
+  cudaFree(h->st_vol[1]);
+  cudaFree(h->st_labels);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
+  }
+}
+
+// Check for an asynchronous fault left by earlier work before enqueueing more.
+hgf_status check_async(hgf_ctx* h) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(h, e, "pending CUDA error");
+  }
+  return HGF_OK;
+}
+
+// Steps 1-2: guidance + label-independent statistics (once per frame).
+hgf_status frame_stats(hgf_ctx* h, const float* guide) {
+  cudaError_t e = hgf::launch_poly_guidance(guide, h->G, h->m, h->d, h->W, h->H, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
+  h->launches++;
+  e = hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "stats");
+  h->launches++;
+  return HGF_OK;
+}
+
+// Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
+hgf_status slices(hgf_ctx* h, const float* vol, int L, int label_offset, float* filtered_out, int do_wta,
+                  int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
+  const long long HW = (long long)h->W * h->H;
+  const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+  for (int c0 = 0; c0 < L; c0 += h->lcap) {
+    const int Lc = (L - c0 < h->lcap) ? (L - c0) : h->lcap;
+    cudaError_t e = hgf::launch_coef(h->n, h->G, h->stats, vol + (long long)c0 * HW, h->wbuf, h->W, h->H, h->r, Lc,
+                                     lam0, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "coef");
+    h->launches++;
+    hgf::AggArgs a{};
+    a.G = h->G;
+    a.wbuf = h->wbuf;
+    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc;
+    a.label_base = label_offset + c0;
+    a.filtered_out = filtered_out ? filtered_out + (long long)c0 * HW : nullptr;
+    a.do_wta = do_wta;
+    a.first = (c0 == 0);
+    a.last = (c0 + Lc >= L);
+    a.best_cost = h->best_cost;
+    a.best_label = h->best_label;
+    a.labels_out = labels_out;
+    a.min_cost_out = min_cost_out;
+    a.keys_out = keys_out;
+    e = hgf::launch_agg(h->n, a, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "agg");
+    h->launches++;
+  }
+  return HGF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hgf_status_string(hgf_status s) {
+  switch (s) {
+    case HGF_OK: return "HGF_OK";
+    case HGF_ERR_INVALID_ARGUMENT: return "HGF_ERR_INVALID_ARGUMENT";
+    case HGF_ERR_UNSUPPORTED: return "HGF_ERR_UNSUPPORTED";
+    case HGF_ERR_OUT_OF_MEMORY: return "HGF_ERR_OUT_OF_MEMORY";
+    case HGF_ERR_CUDA: return "HGF_ERR_CUDA";
+  }
+  return "HGF_ERR_UNKNOWN";
+}
+
+const char* hgf_last_error(hgf_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+int hgf_last_launch_count(hgf_handle h) { return h ? h->launches : 0; }
+
+hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_degree, int radius, double eps,
+                         int mode, void* cuda_stream) {
+  if (!out) return HGF_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (W < 1 || H < 1 || n_guide < 1 || poly_degree < 1 || radius < 1) return HGF_ERR_INVALID_ARGUMENT;
+  if (!(eps > 0.0) || !std::isfinite(eps)) return HGF_ERR_INVALID_ARGUMENT;
+  if (mode != HGF_MODE_HGF && mode != HGF_MODE_GF) return HGF_ERR_INVALID_ARGUMENT;
+  if ((long long)W * H > (1LL << 31)) return HGF_ERR_UNSUPPORTED;
+  if ((long long)n_guide * poly_degree > HGF_MAX_CHANNELS || radius > HGF_MAX_RADIUS) return HGF_ERR_UNSUPPORTED;
+  hgf_ctx* h = new hgf_ctx();
+  h->W = W; h->H = H; h->m = n_guide; h->d = poly_degree; h->n = n_guide * poly_degree;
+  h->r = radius; h->eps = eps; h->mode = mode;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaGetDevice(&h->device);
+  const size_t HW = (size_t)W * H;
+  const int K = h->n + 1;
+  const size_t per_label = (size_t)K * HW * sizeof(float);
+  size_t cap = coef_budget_bytes() / per_label;
+  h->lcap = (int)(cap < 1 ? 1 : (cap > 4096 ? 4096 : cap));
+  cudaError_t e = cudaSuccess;
+  if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
+      (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess ||
+      (e = cudaMalloc(&h->wbuf, per_label * h->lcap)) != cudaSuccess ||
+      (e = cudaMalloc(&h->best_cost, sizeof(float) * HW)) != cudaSuccess ||
+      (e = cudaMalloc(&h->best_label, sizeof(int32_t) * HW)) != cudaSuccess) {
+    cudaGetLastError();
+    release(h);
+    delete h;
+    return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
+  }
+  *out = h;
+  return HGF_OK;
+}
+
+hgf_status hgf_create(hgf_handle* out, int W, int H, int n_guide, int poly_degree, int radius, double eps) {
+  return hgf_create_ex(out, W, H, n_guide, poly_degree, radius, eps, HGF_MODE_HGF, nullptr);
+}
+
+hgf_status hgf_destroy(hgf_handle h) {
+  if (!h) return HGF_OK;
+  cudaStreamSynchronize(h->stream);
+  if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+  release(h);
+  delete h;
+  return HGF_OK;
+}
+
+hgf_status hgf_set_stream(hgf_handle h, void* cuda_stream) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  return HGF_OK;
+}
+
+hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float* dst) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!guide || !src || !dst) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  if (dst == src || dst == guide) return fail(h, HGF_ERR_INVALID_ARGUMENT, "dst aliases an input");
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  if ((s = frame_stats(h, guide)) != HGF_OK) return s;
+  return slices(h, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
+}
+
+hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* cost_volume, int L, int label_offset,
+                                int32_t* labels_out, float* min_cost_out, float* filtered_out, int64_t* keys_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!guide || !cost_volume) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null input pointer");
+  if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
+  if (label_offset < 0 || (long long)label_offset + L > 2147483647LL)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
+  if (!labels_out && !min_cost_out && !filtered_out && !keys_out)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  if ((s = frame_stats(h, guide)) != HGF_OK) return s;
+  const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
+  return slices(h, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
+}
+
+hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {
+  if (!labels_out) return h ? fail(h, HGF_ERR_INVALID_ARGUMENT, "labels_out is null") : HGF_ERR_INVALID_ARGUMENT;
+  return hgf_aggregate_wta_ex(h, guide, cost_volume, L, 0, labels_out, nullptr, nullptr, nullptr);
+}
+
+hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_out, float* min_cost_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!keys || (!labels_out && !min_cost_out)) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaError_t e = hgf::launch_unpack_keys(keys, labels_out, min_cost_out, h->W, h->H, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "unpack_keys");
+  h->launches++;
+  return HGF_OK;
+}
+
+hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const float* cost_host, int L,
+                                  int32_t* labels_host) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!guide_host || !cost_host || !labels_host) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
+  const size_t HW = (size_t)h->W * h->H;
+  cudaError_t e;
+  if (!h->st_guide) {
+    h->st_chunk = h->lcap;
+    if ((e = cudaMalloc(&h->st_guide, sizeof(float) * h->m * HW)) != cudaSuccess ||
+        (e = cudaMalloc(&h->st_vol[0], sizeof(float) * HW * h->st_chunk)) != cudaSuccess ||
+        (e = cudaMalloc(&h->st_vol[1], sizeof(float) * HW * h->st_chunk)) != cudaSuccess ||
+        (e = cudaMalloc(&h->st_labels, sizeof(int32_t) * HW)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(h, e, "staging allocation");
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(h, e, "event creation");
+    }
+  }
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  if ((e = cudaMemcpyAsync(h->st_guide, guide_host, sizeof(float) * h->m * HW, cudaMemcpyHostToDevice, h->stream)) !=
+      cudaSuccess)
+    return cuda_fail(h, e, "guide H2D");
+  if ((s = frame_stats(h, h->st_guide)) != HGF_OK) return s;
+  const long long lcap = h->st_chunk;
+  const int nchunks = (int)((L + lcap - 1) / lcap);
+  const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+  // double-buffered: copy chunk c+1 on copy_stream while chunk c is aggregated on the handle's stream
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    const int l0 = (int)(c * lcap);
+    const int Lc = (int)((L - l0 < lcap) ? (L - l0) : lcap);
+    if (c >= 2 && (e = cudaStreamWaitEvent(h->copy_stream, h->ev_used[b], 0)) != cudaSuccess)
+      return cuda_fail(h, e, "wait used");
+    if ((e = cudaMemcpyAsync(h->st_vol[b], cost_host + (size_t)l0 * HW, sizeof(float) * HW * Lc,
+                             cudaMemcpyHostToDevice, h->copy_stream)) != cudaSuccess)
+      return cuda_fail(h, e, "volume H2D");
+    if ((e = cudaEventRecord(h->ev_copied[b], h->copy_stream)) != cudaSuccess) return cuda_fail(h, e, "record");
+    if ((e = cudaStreamWaitEvent(h->stream, h->ev_copied[b], 0)) != cudaSuccess) return cuda_fail(h, e, "wait copied");
+    e = hgf::launch_coef(h->n, h->G, h->stats, h->st_vol[b], h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "coef");
+    h->launches++;
+    hgf::AggArgs a{};
+    a.G = h->G; a.wbuf = h->wbuf; a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.label_base = l0;
+    a.filtered_out = nullptr; a.do_wta = 1; a.first = (c == 0); a.last = (c == nchunks - 1);
+    a.best_cost = h->best_cost; a.best_label = h->best_label; a.labels_out = h->st_labels;
+    a.min_cost_out = nullptr; a.keys_out = nullptr;
+    if ((e = hgf::launch_agg(h->n, a, h->stream)) != cudaSuccess) return cuda_fail(h, e, "agg");
+    h->launches++;
+    if ((e = cudaEventRecord(h->ev_used[b], h->stream)) != cudaSuccess) return cuda_fail(h, e, "record used");
+  }
+  if ((e = cudaMemcpyAsync(labels_host, h->st_labels, sizeof(int32_t) * HW, cudaMemcpyDeviceToHost, h->stream)) !=
+      cudaSuccess)
+    return cuda_fail(h, e, "labels D2H");
+  if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cuda_fail(h, e, "sync");
+  return HGF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// Internal device helpers for the HGF kernels (sm_100a).  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hgf {
+
+// Clipped-window pixel count N_p = |Omega_p| = B(G_0)(p) (border reading F6).
+__device__ __forceinline__ int window_count(int y, int x, int H, int W, int r) {
+  const int ny = min(y + r, H - 1) - max(y - r, 0) + 1;
+  const int nx = min(x + r, W - 1) - max(x - r, 0) + 1;
+  return ny * nx;
+}
+
+// Monotone float -> uint32 map used by the packed WTA keys (hgf.h, hgf_aggregate_wta_ex).
+__device__ __forceinline__ uint32_t orderable_bits(float f) {
+  f = f + 0.0f;  // canonicalise -0.0 to +0.0
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_orderable_bits(uint32_t o) {
+  const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ uint64_t pack_key(float cost, int32_t label) {
+  return (static_cast<uint64_t>(orderable_bits(cost)) << 32) | static_cast<uint32_t>(label);
+}
+
+// Signed-order key (hgf.h keys_out): unsigned key XOR 2^63, so int64 MIN == unsigned MIN.
+__device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
+  return static_cast<int64_t>(pack_key(cost, label) ^ 0x8000000000000000ull);
+}
+
+// Number of statistics planes stored per pixel for n channels: P' (upper triangle) + nu.
+__host__ __device__ constexpr int stats_planes(int n) { return n * (n + 1) / 2 + n; }
+
+}  // namespace hgf

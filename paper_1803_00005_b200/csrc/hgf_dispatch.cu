@@ -1,0 +1,81 @@
+// Non-template kernels (K1 guidance, key unpacking) and the n -> template dispatch.
+// The per-n template instantiations live in hgf_inst.cu (compiled once per n with -DHGF_N=n).
+#include "hgf_common.cuh"
+#include "hgf_launch.h"
+
+namespace hgf {
+
+// ------------------------------------------------------------------ K1: polynomial guidance
+__global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__ G, int m, int d, long long HW) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
+    for (int i = 0; i < m; ++i) {
+      const float v = I[i * HW + p];
+      float t = v;                       // repeated multiplication: I^1, I^2, ... (exact powers order)
+      G[(long long)(i * d) * HW + p] = t;
+      for (int j = 1; j < d; ++j) {
+        t = t * v;
+        G[(long long)(i * d + j) * HW + p] = t;
+      }
+    }
+  }
+}
+
+__global__ void k_unpack_keys(const int64_t* __restrict__ keys, int32_t* __restrict__ labels, float* __restrict__ cost,
+                              long long HW) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
+    const uint64_t k = (uint64_t)keys[p] ^ 0x8000000000000000ull;
+    if (labels) labels[p] = (int32_t)(uint32_t)(k & 0xffffffffull);
+    if (cost) cost[p] = from_orderable_bits((uint32_t)(k >> 32));
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_1d(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  return (int)(b < 148LL * 32 ? (b < 1 ? 1 : b) : 148LL * 32);
+}
+
+cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st) {
+  const long long HW = (long long)W * H;
+  k_poly_guidance<<<grid_1d(HW, 256), 256, 0, st>>>(I, G, m, d, HW);
+  return cudaGetLastError();
+}
+
+#define HGF_DISPATCH(n, CALL)                                                          \
+  switch (n) {                                                                         \
+    case 1: return CALL(1); case 2: return CALL(2); case 3: return CALL(3);            \
+    case 4: return CALL(4); case 5: return CALL(5); case 6: return CALL(6);            \
+    case 7: return CALL(7); case 8: return CALL(8); case 9: return CALL(9);            \
+    case 10: return CALL(10); case 11: return CALL(11); case 12: return CALL(12);      \
+    case 13: return CALL(13); case 14: return CALL(14); case 15: return CALL(15);      \
+    case 16: return CALL(16); case 17: return CALL(17); case 18: return CALL(18);      \
+    case 19: return CALL(19); case 20: return CALL(20);                                \
+    default: return cudaErrorInvalidValue;                                             \
+  }
+
+cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st) {
+#define CALL(N) stats_impl<N>(G, stats, W, H, r, lam, mode, st)
+  HGF_DISPATCH(n, CALL)
+#undef CALL
+}
+
+cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H, int r,
+                        int L, float lam0, cudaStream_t st) {
+#define CALL(N) coef_impl<N>(G, stats, vol, wbuf, W, H, r, L, lam0, st)
+  HGF_DISPATCH(n, CALL)
+#undef CALL
+}
+
+cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st) {
+#define CALL(N) agg_impl<N>(a, st)
+  HGF_DISPATCH(n, CALL)
+#undef CALL
+}
+
+cudaError_t launch_unpack_keys(const int64_t* keys, int32_t* labels, float* cost, int W, int H, cudaStream_t st) {
+  const long long HW = (long long)W * H;
+  k_unpack_keys<<<grid_1d(HW, 256), 256, 0, st>>>(keys, labels, cost, HW);
+  return cudaGetLastError();
+}
+
+}  // namespace hgf

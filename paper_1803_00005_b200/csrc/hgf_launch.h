@@ -1,0 +1,40 @@
+// Internal launcher interface between the C ABI (hgf_api.cu) and the kernels (hgf_kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hgf {
+
+struct AggArgs {
+  const float* G;
+  const float* wbuf;
+  int W, H, r, L, label_base;
+  float* filtered_out;
+  int do_wta, first, last;
+  float* best_cost;
+  int32_t* best_label;
+  int32_t* labels_out;
+  float* min_cost_out;
+  int64_t* keys_out;
+};
+
+cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st);
+cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode,
+                         cudaStream_t st);
+cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H,
+                        int r, int L, float lam0, cudaStream_t st);
+cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st);
+cudaError_t launch_unpack_keys(const int64_t* keys, int32_t* labels, float* cost, int W, int H, cudaStream_t st);
+
+}  // namespace hgf
+
+namespace hgf {
+// Per-n implementations (defined in hgf_kernels.cuh, instantiated by hgf_inst.cu for n = 1..20).
+template <int NC>
+cudaError_t stats_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st);
+template <int NC>
+cudaError_t coef_impl(const float* G, const float* stats, const float* vol, float* wbuf, int W, int H, int r, int L,
+                      float lam0, cudaStream_t st);
+template <int NC>
+cudaError_t agg_impl(const AggArgs& a, cudaStream_t st);
+}  // namespace hgf

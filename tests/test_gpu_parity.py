@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same seeded inputs."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from tests.parity_util import check_labels, check_z
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _hgf(W, H, m, d, r, lam, mode="hgf"):
+    from paper_1803_00005_b200 import HGF
+    return HGF(W, H, m, d, r, lam, mode=mode)
+
+
+def _run(I, V, d, r, lam, mode="hgf", label_offset=0):
+    torch = _torch()
+    m, H, W = I.shape
+    h = _hgf(W, H, m, d, r, lam, mode)
+    gi = torch.from_numpy(np.ascontiguousarray(I)).cuda()
+    gv = torch.from_numpy(np.ascontiguousarray(V)).cuda()
+    out = h.aggregate_wta_ex(gi, gv, label_offset=label_offset, labels=True, min_cost=True, filtered=True, keys=True)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    res["launches"] = h.last_launch_count
+    h.close()
+    return res
+
+
+CASES = [
+    # (name, W, H, m, d, L, r, lam, mode)
+    ("C1-hgf", 64, 48, 3, 1, 8, 2, 1e-3, "hgf"),
+    ("C1-gf", 64, 48, 3, 1, 8, 2, 1e-3, "gf"),
+    ("ragged-n6", 77, 53, 3, 2, 5, 9, 0.05, "hgf"),
+    ("ragged-n9", 45, 70, 3, 3, 4, 9, 0.05, "hgf"),
+    ("gray-n1", 40, 33, 1, 1, 3, 4, 0.05, "hgf"),
+    ("gray-n3-gf", 40, 33, 1, 3, 3, 3, 0.05, "gf"),
+    ("n20", 36, 20, 10, 2, 2, 5, 0.05, "hgf"),
+    ("r16", 50, 41, 3, 2, 3, 16, 0.05, "hgf"),
+    ("r32-small-image", 20, 17, 3, 2, 3, 32, 0.05, "hgf"),
+    ("one-row", 67, 1, 3, 2, 3, 3, 0.05, "hgf"),
+    ("one-pixel", 1, 1, 3, 2, 4, 2, 0.05, "hgf"),
+    ("L1", 33, 35, 3, 2, 1, 9, 0.05, "hgf"),
+]
+
+
+@pytest.mark.parametrize("name,W,H,m,d,L,r,lam,mode", CASES, ids=[c[0] for c in CASES])
+def test_aggregate_parity(name, W, H, m, d, L, r, lam, mode):
+    seed = sum(name.encode()) % 1000                                   # stable across processes
+    scene = synth.make_stereo_scene(max(W, 8), max(H, 8), max(L, 2), seed=seed)
+    if m == 3:
+        I = scene.left[:, :H, :W]
+    else:
+        I = synth.smooth_guides(W, H, m, seed=7)
+    V = synth.stereo_cost_volume_np(scene, max(L, 2))[:L, :H, :W]
+    I, V = np.ascontiguousarray(I), np.ascontiguousarray(V)
+    res = _run(I, V, d, r, lam, mode)
+    Z = O.hgf_filter(I, V, lam, r, d, mode=mode)
+    s_v = float(np.abs(V).max())
+    check_z(res["filtered"], Z, s_v)
+    check_labels(res["labels"], Z, s_v)
+    # min cost and keys agree with the filtered slices of the same run (bit-exact)
+    lab = res["labels"]
+    assert np.array_equal(res["min_cost"], np.take_along_axis(res["filtered"], lab[None].astype(np.int64), 0)[0])
+    ku = O.pack_keys(res["min_cost"], lab) ^ np.uint64(1 << 63)
+    assert np.array_equal(res["keys"].view(np.uint64), ku)
+
+
+def test_c2_full_parity():
+    """BASELINE config 2 in full: 450x375 Middlebury size, degree-2 RGB (n = 6), 60 labels, r = 9."""
+    c = synth.config("C2")
+    scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
+    V = synth.stereo_cost_volume_np(scene, c["L"])
+    res = _run(scene.left, V, c["d"], c["r"], c["lam"])
+    Z = O.hgf_filter(scene.left, V, c["lam"], c["r"], c["d"])
+    s_v = float(np.abs(V).max())
+    check_z(res["filtered"], Z, s_v)
+    agree, near = check_labels(res["labels"], Z, s_v)
+    assert agree >= 0.9999
+
+
+def test_iid_stress_parity():
+    """'iid' distribution: U[0,1) guide and costs, many near-ties (numerics stress)."""
+    I, V = synth.iid_volume(96, 64, 12, 3, seed=11)
+    res = _run(I, V, 2, 9, 0.05)
+    Z = O.hgf_filter(I, V, 0.05, 9, 2)
+    check_z(res["filtered"], Z, 1.0)
+    check_labels(res["labels"], Z, 1.0)
+
+
+def test_filter_entry_point():
+    torch = _torch()
+    I = synth.smooth_guides(70, 45, 3, seed=3)
+    Y = synth.iid_volume(70, 45, 1, 1, seed=4)[1][0]
+    h = _hgf(70, 45, 3, 2, 7, 0.05)
+    dst = h.filter(torch.from_numpy(I).cuda(), torch.from_numpy(Y).cuda())
+    torch.cuda.synchronize()
+    check_z(dst.cpu().numpy(), O.hgf_filter(I, Y, 0.05, 7, 2), 1.0)
+    h.close()
+
+
+def test_deterministic_and_label_offset_and_permutation():
+    I, V = synth.iid_volume(50, 40, 6, 3, seed=5)
+    a = _run(I, V, 2, 4, 0.05)
+    b = _run(I, V, 2, 4, 0.05, label_offset=100)
+    assert np.array_equal(a["filtered"], b["filtered"])
+    assert np.array_equal(a["labels"] + 100, b["labels"])
+    perm = np.array([3, 0, 5, 1, 4, 2])
+    c = _run(I, np.ascontiguousarray(V[perm]), 2, 4, 0.05)
+    assert np.array_equal(c["filtered"], a["filtered"][perm])          # per-slice arithmetic independent of l
+
+
+def test_chunked_equals_single_chunk(monkeypatch):
+    I, V = synth.iid_volume(512, 300, 5, 3, seed=6)                    # 4.3 MB of coefficients per label
+    a = _run(I, V, 2, 5, 0.05)
+    monkeypatch.setenv("HGF_COEF_BUDGET_MB", "1")                      # 1 MiB -> 1-label chunks
+    b = _run(I, V, 2, 5, 0.05)
+    assert b["launches"] > a["launches"]
+    for k in ("filtered", "labels", "min_cost", "keys"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_shard_merge_equals_unsharded():
+    """Label sharding: per-shard keys, elementwise int64 MIN == unsharded keys (bit-exact)."""
+    torch = _torch()
+    from paper_1803_00005_b200 import shard_range
+    I, V = synth.iid_volume(48, 36, 11, 3, seed=8)
+    full = _run(I, V, 2, 3, 0.05)
+    keys = None
+    for rank in range(3):
+        l0, l1 = shard_range(11, 3, rank)
+        part = _run(I, np.ascontiguousarray(V[l0:l1]), 2, 3, 0.05, label_offset=l0)
+        keys = part["keys"] if keys is None else np.minimum(keys, part["keys"])
+    assert np.array_equal(keys, full["keys"])
+    h = _hgf(48, 36, 3, 2, 3, 0.05)
+    lab, cost = h.unpack_keys(torch.from_numpy(keys).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(lab.cpu().numpy(), full["labels"])
+    assert np.array_equal(cost.cpu().numpy(), full["min_cost"])
+
+
+def test_host_entry_point_matches_device():
+    torch = _torch()
+    I, V = synth.iid_volume(40, 30, 7, 3, seed=9)
+    dev = _run(I, V, 2, 3, 0.05)
+    h = _hgf(40, 30, 3, 2, 3, 0.05)
+    lab = h.aggregate_wta_host(torch.from_numpy(I), torch.from_numpy(V))
+    assert np.array_equal(lab.numpy(), dev["labels"])
+
+
+def test_invalid_arguments_fail_loudly():
+    torch = _torch()
+    from paper_1803_00005_b200 import HGF, HGFError
+    with pytest.raises(HGFError):
+        HGF(10, 10, 3, 2, 2, 0.0)
+    with pytest.raises(HGFError):
+        HGF(10, 10, 11, 2, 2, 0.05)          # n = 22 > HGF_MAX_CHANNELS
+    h = HGF(10, 10, 3, 2, 2, 0.05)
+    with pytest.raises(HGFError):
+        h.aggregate_wta(torch.zeros(3, 10, 10, device="cuda"), torch.zeros(2, 10, 11, device="cuda"))
