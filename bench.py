@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the HGF hot path (BASELINE.json metric): cost-volume voxels/s aggregated + WTA.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl own|reference]
+Under torchrun (N > 1): one rank per GPU, labels sharded contiguously, keys merged by NCCL
+allreduce-MIN.  Rank 0 prints ONE JSON line.  A "step" = one pass of the whole hot path over one
+synthetic frame: guidance -> float64 statistics -> every label slice filtered -> WTA (-> merge).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cost-volume voxels/sec aggregated+WTA; achieved HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "voxels/s"
+SM_COUNT = 148
+FP32_LANES = 128
+FP64_LANES = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=64)
+    ap.add_argument("--cpu-sample-labels", type=int, default=32)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- algorithmic work
+def alg_flops_per_voxel(n):
+    """Per voxel (fp32), as counted in DESIGN.md §5: coef 2n^2+9n+5, agg 6n+6."""
+    return {"coef": 2 * n * n + 9 * n + 5, "agg": 6 * n + 6}
+
+
+def alg_flops_stats_per_pixel(n):
+    """fp64 per pixel: Gram (1 mul + 4 adds per product plane) + Prop-1 recursion."""
+    K = n + 1
+    gram = 5 * (K * (K + 1) // 2 - 1)
+    rec = sum(2 * k * k + 2 * k + 3 * k * k + 2 * k + 6 for k in range(1, K))
+    return gram + rec
+
+
+def alg_bytes(W, H, L, m):
+    """HBM bytes the pass must move: the cost volume once, the guide once, the labels once."""
+    return 4 * W * H * L + 4 * m * W * H + 4 * W * H
+
+
+def workload_name(c):
+    return (f"{c['name']}: {c['W']}x{c['H']} stereo-like v1, RGB degree-{c['d']} polynomial guidance (n={c['n']}), "
+            f"{c['L']} labels, r={c['r']}, lambda={c['lam']}, HGF mode")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle sample
+def oracle_sample(scene_left, vol_band_np, c, y0, rows, halo_top):
+    """Time the float64 oracle on a row band (with 2r halos) of the workload; returns (voxels, seconds)."""
+    import numpy as np
+
+    import oracle as O
+    t = time.perf_counter()
+    I = scene_left
+    Z = O.hgf_filter(I, vol_band_np, c["lam"], c["r"], c["d"])
+    lab = np.argmin(Z, axis=0)
+    dt = time.perf_counter() - t
+    _ = lab[halo_top:halo_top + rows]
+    return rows * vol_band_np.shape[2] * vol_band_np.shape[0], dt
+
+
+def make_band(scene, c, y0, rows, labels):
+    import numpy as np
+
+    import synth
+    r2 = 2 * c["r"]
+    ya, yb = max(0, y0 - r2), min(c["H"], y0 + rows + r2)
+    sub = synth.StereoScene(np.ascontiguousarray(scene.left[:, ya:yb]), np.ascontiguousarray(scene.right[:, ya:yb]),
+                            scene.disp[ya:yb])
+    V = synth.stereo_cost_volume_np(sub, c["L"], 0, labels)
+    return sub.left, V, y0 - ya
+
+
+def cpu_baseline(scene, c, rows, labels, y0=None):
+    y0 = c["H"] // 2 if y0 is None else y0
+    rows = min(rows, c["H"])
+    y0 = min(y0, c["H"] - rows)
+    labels = min(labels, c["L"])
+    I, V, halo = make_band(scene, c, y0, rows, labels)
+    vox, dt = oracle_sample(I, V, c, y0, rows, halo)
+    return {"value": vox / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"rows {y0}-{y0 + rows - 1} (+{2 * c['r']}-row halos) x {c['W']} cols x labels 0-{labels - 1} "
+                       f"of {c['name']}: {vox} voxels in {dt:.2f} s, numpy float64, 1 thread")}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import synth
+    scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
+    rows, labels = 16, 8
+    vals = []
+    for i in range(args.warmup + args.steps):
+        y0 = (i * 97) % max(1, c["H"] - rows)
+        I, V, halo = make_band(scene, c, y0, rows, labels)
+        vox, dt = oracle_sample(I, V, c, y0, rows, halo)
+        if i >= args.warmup:
+            vals.append((vox, dt))
+    vox = sum(v for v, _ in vals)
+    sec = sum(d for _, d in vals)
+    value = vox / sec
+    sample = (f"per step: a {rows}-row band (+{2 * c['r']}-row halos) x {c['W']} cols x {labels} labels of "
+              f"{c['name']} (band start varies per step); float64 numpy oracle, 1 thread")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / len(vals),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (stereo-like v1, seeded)", "config": config_json(c, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_json(c, n_gpus):
+    return {"workload": workload_name(c), "W": c["W"], "H": c["H"], "labels": c["L"], "n_guide": c["m"],
+            "poly_degree": c["d"], "n": c["n"], "radius": c["r"], "lambda": c["lam"],
+            "parallelism": f"label-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2 (cost volume > 126 MB); no flush needed"}
+
+
+# ----------------------------------------------------------------------------- own arm
+def main():
+    args = parse()
+    import synth
+    c = synth.config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, c)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_00005_b200 import HGF, merge_keys_allreduce, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W, H, L, m, d, r, lam = c["W"], c["H"], c["L"], c["m"], c["d"], c["r"], c["lam"]
+    n = c["n"]
+    l0, l1 = shard_range(L, world, rank)
+    Ls = l1 - l0
+    scene = synth.make_stereo_scene(W, H, L, c["seed"])
+    guide = torch.from_numpy(scene.left).to(dev)
+    vol = synth.stereo_cost_volume_torch(scene, L, dev, l0, l1)
+    torch.cuda.synchronize()
+    h = HGF(W, H, m, d, r, lam)
+    labels = torch.empty((H, W), dtype=torch.int32, device=dev)
+    keys = torch.empty((H, W), dtype=torch.int64, device=dev)
+    mincost = torch.empty((H, W), dtype=torch.float32, device=dev)
+
+    def step():
+        if world == 1:
+            h.aggregate_wta(guide, vol, labels)
+        else:
+            h.aggregate_wta_ex(guide, vol, label_offset=l0, labels=False, keys=True, out={"keys": keys})
+            merge_keys_allreduce(keys)
+            h.unpack_keys(keys, labels, mincost)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    h.profile_read()
+    h.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    prof = h.profile_read()
+    h.set_profiling(False)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    launches = sum(cnt for _, cnt in prof.values())
+    lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    voxels = W * H * L * args.steps
+    value = voxels / (ms_max / 1e3)
+
+    # roofline of the dominant kernel class (largest device time inside the timed region)
+    fl = alg_flops_per_voxel(n)
+    dom = max(("coef", "agg", "stats"), key=lambda k: prof[k][0])
+    dom_ms, dom_cnt = prof[dom]
+    if dom in ("coef", "agg"):
+        flops_total = fl[dom] * W * H * Ls * args.steps
+        peak = SM_COUNT * FP32_LANES * 2 * 1965e6 / 1e12
+    else:
+        flops_total = alg_flops_stats_per_pixel(n) * W * H * args.steps
+        peak = SM_COUNT * FP64_LANES * 2 * 1965e6 / 1e12
+    achieved = flops_total / dom_cnt / (dom_ms / dom_cnt / 1e3) / 1e12 if dom_cnt else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            ent = tj.get(c["name"], {}).get(dom)
+            if ent is not None:
+                traffic = ent
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": {"coef": "k_coef", "agg": "k_agg", "stats": "k_stats"}[dom],
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_basis": ("148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts/clock)"
+                               if dom != "stats" else "148 SMs x 64 FP64 lanes x 2 x 1965 MHz"),
+                "share_of_step": dom_ms / (ms_max if world == 1 else ms) if ms else None}
+    stage_ms = {k: v[0] / args.steps for k, v in prof.items()}
+    hbm_peak = 6536.0
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    hbm_ach = alg_bytes(W, H, L, m) * args.steps / (ms_max / 1e3) / 1e9
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        if world == 1:
+            vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
+            vol_h.copy_(vol)
+            guide_h = torch.from_numpy(scene.left).pin_memory()
+            lab_h = torch.empty((H, W), dtype=torch.int32, pin_memory=True)
+            h.aggregate_wta_host(guide_h, vol_h, lab_h)          # warm-up (allocates staging)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                h.aggregate_wta_host(guide_h, vol_h, lab_h)
+            dt = time.perf_counter() - t0
+            e2e = {"value": W * H * L * args.e2e_steps / dt, "unit": UNIT,
+                   "h2d_bytes_per_step": vol_h.numel() * 4 + guide_h.numel() * 4, "d2h_bytes_per_step": lab_h.numel() * 4,
+                   "api": "hgf_aggregate_wta_host (chunked H2D overlapped with compute)"}
+            del vol_h
+        else:
+            vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
+            vol_h.copy_(vol)
+            guide_h = torch.from_numpy(scene.left).pin_memory()
+            lab_h = torch.empty((H, W), dtype=torch.int32, pin_memory=True)
+
+            def e2e_step():
+                vol.copy_(vol_h, non_blocking=True)
+                guide.copy_(guide_h, non_blocking=True)
+                step()
+                if rank == 0:
+                    lab_h.copy_(labels, non_blocking=True)
+                torch.cuda.synchronize()
+
+            e2e_step()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                e2e_step()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            e2e = {"value": W * H * L * args.e2e_steps / float(dt.item()), "unit": UNIT,
+                   "h2d_bytes_per_step": 4 * W * H * L + 4 * m * W * H * world, "d2h_bytes_per_step": 4 * W * H,
+                   "api": "torch H2D copies + HGF.aggregate_wta_ex + NCCL allreduce-MIN + HGF.unpack_keys"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        cpu = cpu_baseline(scene, c, args.cpu_sample_rows, args.cpu_sample_labels)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (stereo-like v1 generator, seeded; cost volume built in HBM before timing)",
+                "config": config_json(c, world), "roofline": roofline,
+                "hbm": {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
+                        "alg_bytes_per_step": alg_bytes(W, H, L, m)},
+                "stage_ms_per_step": stage_ms, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(lt.item()), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

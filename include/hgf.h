@@ -123,6 +123,25 @@ HGF_API hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* l
 HGF_API hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const float* cost_host, int L,
                                   int32_t* labels_host);
 
+/* Kernel classes reported by the tracing calls below. */
+enum {
+  HGF_KC_GUIDANCE = 0, /* K1 polynomial guidance                 */
+  HGF_KC_STATS = 1,    /* K3 float64 Gram + Prop-1 statistics    */
+  HGF_KC_COEF = 2,     /* K4a per-slice coefficients w           */
+  HGF_KC_AGG = 3,      /* K4b per-slice aggregation Z + WTA      */
+  HGF_KC_KEYS = 4,     /* key unpacking                          */
+  HGF_KC_COUNT = 5
+};
+
+/* Tracing: when enable != 0, every kernel launch of this handle is bracketed by CUDA events recorded
+ * on the handle's stream (a few microseconds of host overhead per launch; no device synchronisation). */
+HGF_API hgf_status hgf_set_profiling(hgf_handle h, int enable);
+
+/* Synchronise the handle's stream, then write the device time (ms) and launch count accumulated per
+ * kernel class since the previous read into ms[0..n) and counts[0..n) (either may be NULL; n <=
+ * HGF_KC_COUNT), and reset the accumulators. */
+HGF_API hgf_status hgf_profile_read(hgf_handle h, double* ms, int* counts, int n);
+
 /* Number of kernel launches the last hgf_filter / hgf_aggregate_wta* call enqueued. */
 HGF_API int hgf_last_launch_count(hgf_handle h);
 

@@ -22,8 +22,9 @@ lib_path = os.path.join(_HERE, "libhgf.so")
 EXPORTED_SYMBOLS = (
     "hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter",
     "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
-    "hgf_last_launch_count", "hgf_status_string", "hgf_last_error",
+    "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
 )
+KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys")   # HGF_KC_* order
 
 _lib = None
 
@@ -56,6 +57,10 @@ def lib():
     L.hgf_status_string.restype = ctypes.c_char_p
     L.hgf_last_error.argtypes = [vp]
     L.hgf_last_error.restype = ctypes.c_char_p
+    L.hgf_set_profiling.argtypes = [vp, c_int]
+    L.hgf_set_profiling.restype = c_int
+    L.hgf_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int), c_int]
+    L.hgf_profile_read.restype = c_int
     for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
                  "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host"):
         getattr(L, name).restype = c_int
@@ -105,6 +110,18 @@ class HGF:
         if tuple(t.shape) != tuple(shape):
             raise HGFError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
         return t
+
+    def set_profiling(self, enable=True):
+        self._check(lib().hgf_set_profiling(self._h, 1 if enable else 0), "hgf_set_profiling")
+
+    def profile_read(self):
+        """{class: (ms, launches)} accumulated since the previous read (synchronises the stream)."""
+        n = len(KERNEL_CLASSES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int * n)()
+        self._bind_stream()
+        self._check(lib().hgf_profile_read(self._h, ms, cnt, n), "hgf_profile_read")
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
 
     @property
     def last_launch_count(self):

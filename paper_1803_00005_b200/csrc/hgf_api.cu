@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "../../include/hgf.h"
 #include "hgf_common.cuh"
@@ -30,6 +31,11 @@ struct hgf_ctx {
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int launches = 0;
   std::string err;
+  // tracing (hgf_set_profiling / hgf_profile_read)
+  bool profiling = false;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;        // recorded since the last read
+  std::vector<cudaEvent_t> pool;
 };
 
 namespace {
@@ -43,12 +49,34 @@ hgf_status cuda_fail(hgf_ctx* h, cudaError_t e, const char* where) {
   return fail(h, HGF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-#define HGF_CK(h, expr)                                   \
-  do {                                                    \
-    cudaError_t e_ = (expr);                              \
-    if (e_ != cudaSuccess) return cuda_fail(h, e_, #expr); \
-    (h)->launches++;                                      \
-  } while (0)
+cudaEvent_t take_event(hgf_ctx* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Launch wrapper: counts launches and, when tracing, brackets the launch with events.
+template <class F>
+cudaError_t traced(hgf_ctx* h, int cls, cudaStream_t st, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (h->profiling) {
+    a = take_event(h);
+    b = take_event(h);
+    cudaEventRecord(a, st);
+  }
+  cudaError_t e = f();
+  if (h->profiling) {
+    cudaEventRecord(b, st);
+    h->recs.push_back({cls, a, b});
+  }
+  if (e == cudaSuccess) h->launches++;
+  return e;
+}
 
 size_t coef_budget_bytes() {
   const char* s = std::getenv("HGF_COEF_BUDGET_MB");
@@ -58,6 +86,10 @@ size_t coef_budget_bytes() {
 }
 
 void release(hgf_ctx* h) {
+  for (auto& r : h->recs) { h->pool.push_back(r.a); h->pool.push_back(r.b); }
+  h->recs.clear();
+  for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
+  h->pool.clear();
   cudaFree(h->G);
   cudaFree(h->stats);
   cudaFree(h->wbuf);
@@ -86,12 +118,14 @@ hgf_status check_async(hgf_ctx* h) {
 
 // Steps 1-2: guidance + label-independent statistics (once per frame).
 hgf_status frame_stats(hgf_ctx* h, const float* guide) {
-  cudaError_t e = hgf::launch_poly_guidance(guide, h->G, h->m, h->d, h->W, h->H, h->stream);
+  cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
+    return hgf::launch_poly_guidance(guide, h->G, h->m, h->d, h->W, h->H, h->stream);
+  });
   if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
-  h->launches++;
-  e = hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->stream);
+  e = traced(h, HGF_KC_STATS, h->stream, [&] {
+    return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->stream);
+  });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
-  h->launches++;
   return HGF_OK;
 }
 
@@ -102,10 +136,11 @@ hgf_status slices(hgf_ctx* h, const float* vol, int L, int label_offset, float* 
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   for (int c0 = 0; c0 < L; c0 += h->lcap) {
     const int Lc = (L - c0 < h->lcap) ? (L - c0) : h->lcap;
-    cudaError_t e = hgf::launch_coef(h->n, h->G, h->stats, vol + (long long)c0 * HW, h->wbuf, h->W, h->H, h->r, Lc,
-                                     lam0, h->stream);
+    cudaError_t e = traced(h, HGF_KC_COEF, h->stream, [&] {
+      return hgf::launch_coef(h->n, h->G, h->stats, vol + (long long)c0 * HW, h->wbuf, h->W, h->H, h->r, Lc, lam0,
+                              h->stream);
+    });
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
-    h->launches++;
     hgf::AggArgs a{};
     a.G = h->G;
     a.wbuf = h->wbuf;
@@ -120,9 +155,8 @@ hgf_status slices(hgf_ctx* h, const float* vol, int L, int label_offset, float* 
     a.labels_out = labels_out;
     a.min_cost_out = min_cost_out;
     a.keys_out = keys_out;
-    e = hgf::launch_agg(h->n, a, h->stream);
+    e = traced(h, HGF_KC_AGG, h->stream, [&] { return hgf::launch_agg(h->n, a, h->stream); });
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
-    h->launches++;
   }
   return HGF_OK;
 }
@@ -239,9 +273,10 @@ hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_ou
   h->launches = 0;
   h->err.clear();
   if (!keys || (!labels_out && !min_cost_out)) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
-  cudaError_t e = hgf::launch_unpack_keys(keys, labels_out, min_cost_out, h->W, h->H, h->stream);
+  cudaError_t e = traced(h, HGF_KC_KEYS, h->stream, [&] {
+    return hgf::launch_unpack_keys(keys, labels_out, min_cost_out, h->W, h->H, h->stream);
+  });
   if (e != cudaSuccess) return cuda_fail(h, e, "unpack_keys");
-  h->launches++;
   return HGF_OK;
 }
 
@@ -289,22 +324,52 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
       return cuda_fail(h, e, "volume H2D");
     if ((e = cudaEventRecord(h->ev_copied[b], h->copy_stream)) != cudaSuccess) return cuda_fail(h, e, "record");
     if ((e = cudaStreamWaitEvent(h->stream, h->ev_copied[b], 0)) != cudaSuccess) return cuda_fail(h, e, "wait copied");
-    e = hgf::launch_coef(h->n, h->G, h->stats, h->st_vol[b], h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
+    e = traced(h, HGF_KC_COEF, h->stream, [&] {
+      return hgf::launch_coef(h->n, h->G, h->stats, h->st_vol[b], h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
+    });
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
-    h->launches++;
     hgf::AggArgs a{};
     a.G = h->G; a.wbuf = h->wbuf; a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.label_base = l0;
     a.filtered_out = nullptr; a.do_wta = 1; a.first = (c == 0); a.last = (c == nchunks - 1);
     a.best_cost = h->best_cost; a.best_label = h->best_label; a.labels_out = h->st_labels;
     a.min_cost_out = nullptr; a.keys_out = nullptr;
-    if ((e = hgf::launch_agg(h->n, a, h->stream)) != cudaSuccess) return cuda_fail(h, e, "agg");
-    h->launches++;
+    e = traced(h, HGF_KC_AGG, h->stream, [&] { return hgf::launch_agg(h->n, a, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(h, e, "agg");
     if ((e = cudaEventRecord(h->ev_used[b], h->stream)) != cudaSuccess) return cuda_fail(h, e, "record used");
   }
   if ((e = cudaMemcpyAsync(labels_host, h->st_labels, sizeof(int32_t) * HW, cudaMemcpyDeviceToHost, h->stream)) !=
       cudaSuccess)
     return cuda_fail(h, e, "labels D2H");
   if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cuda_fail(h, e, "sync");
+  return HGF_OK;
+}
+
+hgf_status hgf_set_profiling(hgf_handle h, int enable) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->profiling = enable != 0;
+  return HGF_OK;
+}
+
+hgf_status hgf_profile_read(hgf_handle h, double* ms, int* counts, int n) {
+  if (!h || n < 0 || n > HGF_KC_COUNT) return HGF_ERR_INVALID_ARGUMENT;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "profile sync");
+  double acc[HGF_KC_COUNT] = {0};
+  int cnt[HGF_KC_COUNT] = {0};
+  for (auto& r : h->recs) {
+    float t = 0.0f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      acc[r.cls] += t;
+      cnt[r.cls] += 1;
+    }
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (counts) counts[i] = cnt[i];
+  }
   return HGF_OK;
 }
 
