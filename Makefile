@@ -8,7 +8,8 @@ PKG := paper_1803_00005_b200
 CS := $(PKG)/csrc
 NS := 1 2 3 4 5 6 7 8 9 10 11 12 13 14 15 16 17 18 19 20
 DEPS := $(wildcard $(CS)/*.cuh) $(wildcard $(CS)/*.h) include/hgf.h
-OBJ := build/hgf_api.o build/hgf_dispatch.o $(foreach n,$(NS),build/inst_$(n).o)
+MDS := 1_1 1_2 1_3 2_1 2_2 2_3 3_1 3_2 3_3
+OBJ := build/hgf_api.o build/hgf_dispatch.o $(foreach n,$(NS),build/inst_$(n).o) $(foreach md,$(MDS),build/inst2_$(md).o)
 LIB := $(PKG)/libhgf.so
 
 all: $(LIB)
@@ -20,6 +21,10 @@ build/hgf_%.o: $(CS)/hgf_%.cu $(DEPS)
 build/inst_%.o: $(CS)/hgf_inst.cu $(DEPS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -DHGF_N=$* -c $< -o $@
+
+build/inst2_%.o: $(CS)/hgf_inst2.cu $(DEPS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DHGF_M=$(word 1,$(subst _, ,$*)) -DHGF_D=$(word 2,$(subst _, ,$*)) -c $< -o $@
 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)

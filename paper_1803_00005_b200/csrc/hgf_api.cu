@@ -30,6 +30,7 @@ struct hgf_ctx {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int launches = 0;
+  bool fast = false;           // v2 fast-path kernels usable for (m, d, r)
   std::string err;
   // tracing (hgf_set_profiling / hgf_profile_read)
   bool profiling = false;
@@ -129,17 +130,30 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
   return HGF_OK;
 }
 
-// Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
-hgf_status slices(hgf_ctx* h, const float* vol, int L, int label_offset, float* filtered_out, int do_wta,
-                  int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
-  const long long HW = (long long)h->W * h->H;
+// K4a for one chunk of Lc slices: the v2 fast path when (m, d, r) allow it, else the generic v1 kernel.
+cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+  return traced(h, HGF_KC_COEF, h->stream, [&] {
+    if (h->fast)
+      return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->W, h->H, h->r, Lc, lam0,
+                                   h->stream);
+    return hgf::launch_coef(h->n, h->G, h->stats, vol_chunk, h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
+  });
+}
+
+cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
+  return traced(h, HGF_KC_AGG, h->stream, [&] {
+    return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
+  });
+}
+
+// Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
+hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
+                  int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
+  const long long HW = (long long)h->W * h->H;
   for (int c0 = 0; c0 < L; c0 += h->lcap) {
     const int Lc = (L - c0 < h->lcap) ? (L - c0) : h->lcap;
-    cudaError_t e = traced(h, HGF_KC_COEF, h->stream, [&] {
-      return hgf::launch_coef(h->n, h->G, h->stats, vol + (long long)c0 * HW, h->wbuf, h->W, h->H, h->r, Lc, lam0,
-                              h->stream);
-    });
+    cudaError_t e = launch_coef_chunk(h, guide, vol + (long long)c0 * HW, Lc);
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
     a.G = h->G;
@@ -155,7 +169,7 @@ hgf_status slices(hgf_ctx* h, const float* vol, int L, int label_offset, float* 
     a.labels_out = labels_out;
     a.min_cost_out = min_cost_out;
     a.keys_out = keys_out;
-    e = traced(h, HGF_KC_AGG, h->stream, [&] { return hgf::launch_agg(h->n, a, h->stream); });
+    e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
   }
   return HGF_OK;
@@ -199,6 +213,10 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   const size_t per_label = (size_t)K * HW * sizeof(float);
   size_t cap = coef_budget_bytes() / per_label;
   h->lcap = (int)(cap < 1 ? 1 : (cap > 4096 ? 4096 : cap));
+  {
+    const char* f = std::getenv("HGF_FORCE_V1");
+    h->fast = hgf::fast_path_ok(h->m, h->d, h->r) && !(f && f[0] == '1');
+  }
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
       (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess ||
@@ -242,7 +260,7 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   if ((s = frame_stats(h, guide)) != HGF_OK) return s;
-  return slices(h, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
+  return slices(h, guide, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
 }
 
 hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* cost_volume, int L, int label_offset,
@@ -260,7 +278,7 @@ hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* c
   if (s != HGF_OK) return s;
   if ((s = frame_stats(h, guide)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
-  return slices(h, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
+  return slices(h, guide, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {
@@ -324,16 +342,14 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
       return cuda_fail(h, e, "volume H2D");
     if ((e = cudaEventRecord(h->ev_copied[b], h->copy_stream)) != cudaSuccess) return cuda_fail(h, e, "record");
     if ((e = cudaStreamWaitEvent(h->stream, h->ev_copied[b], 0)) != cudaSuccess) return cuda_fail(h, e, "wait copied");
-    e = traced(h, HGF_KC_COEF, h->stream, [&] {
-      return hgf::launch_coef(h->n, h->G, h->stats, h->st_vol[b], h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
-    });
+    e = launch_coef_chunk(h, h->st_guide, h->st_vol[b], Lc);
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
     a.G = h->G; a.wbuf = h->wbuf; a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.label_base = l0;
     a.filtered_out = nullptr; a.do_wta = 1; a.first = (c == 0); a.last = (c == nchunks - 1);
     a.best_cost = h->best_cost; a.best_label = h->best_label; a.labels_out = h->st_labels;
     a.min_cost_out = nullptr; a.keys_out = nullptr;
-    e = traced(h, HGF_KC_AGG, h->stream, [&] { return hgf::launch_agg(h->n, a, h->stream); });
+    e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
     if ((e = cudaEventRecord(h->ev_used[b], h->stream)) != cudaSuccess) return cuda_fail(h, e, "record used");
   }

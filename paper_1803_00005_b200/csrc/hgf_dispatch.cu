@@ -79,3 +79,35 @@ cudaError_t launch_unpack_keys(const int64_t* keys, int32_t* labels, float* cost
 }
 
 }  // namespace hgf
+
+namespace hgf {
+
+// Must match v2::RMAX in hgf_slice_v2.cuh (register arrays of k_agg2 are sized by it).
+constexpr int kV2RMax = 9;
+
+bool fast_path_ok(int m, int d, int r) { return m >= 1 && m <= 3 && d >= 1 && d <= 3 && r >= 1 && r <= kV2RMax; }
+
+cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf,
+                             int W, int H, int r, int L, float lam0, cudaStream_t st) {
+#define C2(M, D) return v2::coef2_impl<M, D>(guide, stats, vol, wbuf, W, H, r, L, lam0, st)
+  switch (m * 10 + d) {
+    case 11: C2(1, 1); case 12: C2(1, 2); case 13: C2(1, 3);
+    case 21: C2(2, 1); case 22: C2(2, 2); case 23: C2(2, 3);
+    case 31: C2(3, 1); case 32: C2(3, 2); case 33: C2(3, 3);
+    default: return cudaErrorInvalidValue;
+  }
+#undef C2
+}
+
+cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st) {
+  switch (n) {
+    case 1: return v2::agg2_impl<1>(a, st); case 2: return v2::agg2_impl<2>(a, st);
+    case 3: return v2::agg2_impl<3>(a, st); case 4: return v2::agg2_impl<4>(a, st);
+    case 5: return v2::agg2_impl<5>(a, st); case 6: return v2::agg2_impl<6>(a, st);
+    case 7: return v2::agg2_impl<7>(a, st); case 8: return v2::agg2_impl<8>(a, st);
+    case 9: return v2::agg2_impl<9>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hgf

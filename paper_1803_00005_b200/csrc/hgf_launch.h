@@ -38,3 +38,18 @@ cudaError_t coef_impl(const float* G, const float* stats, const float* vol, floa
 template <int NC>
 cudaError_t agg_impl(const AggArgs& a, cudaStream_t st);
 }  // namespace hgf
+
+namespace hgf {
+namespace v2 {
+// Fast path (n_guide <= 3, degree <= 3, radius <= 9): hgf_slice_v2.cuh, instantiated by hgf_inst.cu / hgf_inst2.cu.
+template <int M, int D>
+cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, int W, int H, int r,
+                       int L, float lam0, cudaStream_t st);
+template <int NC>
+cudaError_t agg2_impl(const AggArgs& a, cudaStream_t st);
+}  // namespace v2
+bool fast_path_ok(int m, int d, int r);
+cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf,
+                             int W, int H, int r, int L, float lam0, cudaStream_t st);
+cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st);
+}  // namespace hgf
