@@ -6,6 +6,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/hgf.h"
 #include "hgf_common.cuh"
 #include "hgf_launch.h"
@@ -31,6 +34,9 @@ struct hgf_ctx {
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int launches = 0;
   bool fast = false;           // v2 fast-path kernels usable for (m, d, r)
+  bool v3agg = false;          // TMA-fed v3 aggregation usable (n <= 9, r <= 9, W % 4 == 0)
+  CUtensorMap tm_w;            // TMA descriptor over wbuf (padded layout), box agg3_box(r) x (n+1)
+  hgf::WLayout wlay{};         // coefficient-buffer layout (zero top/left margin of r when v3agg)
   std::string err;
   // tracing (hgf_set_profiling / hgf_profile_read)
   bool profiling = false;
@@ -135,7 +141,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
     if (h->fast)
-      return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->W, h->H, h->r, Lc, lam0,
+      return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                    h->stream);
     return hgf::launch_coef(h->n, h->G, h->stats, vol_chunk, h->wbuf, h->W, h->H, h->r, Lc, lam0, h->stream);
   });
@@ -143,8 +149,33 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
 
 cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
   return traced(h, HGF_KC_AGG, h->stream, [&] {
+    if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, &h->tm_w, a, h->stream);
     return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
   });
+}
+
+// TMA descriptor over the coefficient buffer for the v3 aggregation kernel (driver entry point via the
+// runtime, so the library does not link libcuda directly).
+bool make_wbuf_tensor_map(hgf_ctx* h) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      !fn || q != cudaDriverEntryPointSuccess)
+    return false;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  int bx = 0, by = 0;
+  hgf::agg3_box(h->r, &bx, &by);
+  // padded layout: the image occupies rows/cols [r, r+H) x [r, r+W); the margin is zero, so a tile whose
+  // window starts at (x0 - r, y0 - r) is fetched at the non-negative TMA coordinate (x0, y0).
+  const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->r), (cuuint64_t)(h->H + h->r),
+                              (cuuint64_t)h->lcap * (h->n + 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)(h->n + 1)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(&h->tm_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->wbuf, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 // Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
@@ -210,23 +241,37 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   cudaGetDevice(&h->device);
   const size_t HW = (size_t)W * H;
   const int K = h->n + 1;
-  const size_t per_label = (size_t)K * HW * sizeof(float);
-  size_t cap = coef_budget_bytes() / per_label;
-  h->lcap = (int)(cap < 1 ? 1 : (cap > 4096 ? 4096 : cap));
   {
     const char* f = std::getenv("HGF_FORCE_V1");
     h->fast = hgf::fast_path_ok(h->m, h->d, h->r) && !(f && f[0] == '1');
+    const char* g = std::getenv("HGF_NO_V3");
+    h->v3agg = h->fast && h->n <= 9 && !(g && g[0] == '1');     // confirmed below once the TMA map exists
   }
+  // coefficient buffer layout: padded (zero margin of r rows/cols above/left) for the TMA path
+  const hgf::WLayout flat{0, (long long)HW, W};
+  hgf::WLayout padded{};
+  padded.pitch = (W + h->r + 3) / 4 * 4;
+  padded.plane = (long long)(H + h->r) * padded.pitch;
+  padded.origin = (long long)h->r * padded.pitch + h->r;
+  h->wlay = h->v3agg ? padded : flat;
+  const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
+  size_t cap = coef_budget_bytes() / per_label;
+  h->lcap = (int)(cap < 1 ? 1 : (cap > 4096 ? 4096 : cap));
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
       (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess ||
       (e = cudaMalloc(&h->wbuf, per_label * h->lcap)) != cudaSuccess ||
       (e = cudaMalloc(&h->best_cost, sizeof(float) * HW)) != cudaSuccess ||
-      (e = cudaMalloc(&h->best_label, sizeof(int32_t) * HW)) != cudaSuccess) {
+      (e = cudaMalloc(&h->best_label, sizeof(int32_t) * HW)) != cudaSuccess ||
+      (e = cudaMemset(h->wbuf, 0, per_label * h->lcap)) != cudaSuccess) {
     cudaGetLastError();
     release(h);
     delete h;
     return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
+  }
+  if (h->v3agg && !((long long)h->lcap * K <= (1LL << 31) && make_wbuf_tensor_map(h))) {
+    h->v3agg = false;   // no TMA descriptor: the v2 aggregation reads the flat layout (fits the allocation)
+    h->wlay = flat;
   }
   *out = h;
   return HGF_OK;

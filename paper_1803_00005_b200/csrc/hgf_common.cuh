@@ -31,6 +31,15 @@ __device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
   return static_cast<int64_t>(pack_key(cost, label) ^ 0x8000000000000000ull);
 }
 
+// Layout of the per-slice coefficient buffer: element (label l, plane k, y, x) of a chunk lives at
+// origin + (l*(n+1) + k)*plane + y*pitch + x.  The v3 aggregation pads it with a zero top/left margin
+// (TMA tiles are then fetched at non-negative coordinates).
+struct WLayout {
+  long long origin;
+  long long plane;
+  int pitch;
+};
+
 // Number of statistics planes stored per pixel for n channels: P' (upper triangle) + nu.
 __host__ __device__ constexpr int stats_planes(int n) { return n * (n + 1) / 2 + n; }
 

@@ -87,9 +87,9 @@ constexpr int kV2RMax = 9;
 
 bool fast_path_ok(int m, int d, int r) { return m >= 1 && m <= 3 && d >= 1 && d <= 3 && r >= 1 && r <= kV2RMax; }
 
-cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf,
+cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo,
                              int W, int H, int r, int L, float lam0, cudaStream_t st) {
-#define C2(M, D) return v2::coef2_impl<M, D>(guide, stats, vol, wbuf, W, H, r, L, lam0, st)
+#define C2(M, D) return v2::coef2_impl<M, D>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st)
   switch (m * 10 + d) {
     case 11: C2(1, 1); case 12: C2(1, 2); case 13: C2(1, 3);
     case 21: C2(2, 1); case 22: C2(2, 2); case 23: C2(2, 3);
@@ -106,6 +106,37 @@ cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st) {
     case 5: return v2::agg2_impl<5>(a, st); case 6: return v2::agg2_impl<6>(a, st);
     case 7: return v2::agg2_impl<7>(a, st); case 8: return v2::agg2_impl<8>(a, st);
     case 9: return v2::agg2_impl<9>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hgf
+
+namespace hgf {
+
+template <int NC>
+static cudaError_t agg3_r(int r, const void* tmap, const AggArgs& a, cudaStream_t st) {
+  switch (r) {
+    case 1: return v3::agg3_impl<NC, 1>(tmap, a, st);
+    case 2: return v3::agg3_impl<NC, 2>(tmap, a, st);
+    case 3: return v3::agg3_impl<NC, 3>(tmap, a, st);
+    case 4: return v3::agg3_impl<NC, 4>(tmap, a, st);
+    case 5: return v3::agg3_impl<NC, 5>(tmap, a, st);
+    case 6: return v3::agg3_impl<NC, 6>(tmap, a, st);
+    case 7: return v3::agg3_impl<NC, 7>(tmap, a, st);
+    case 8: return v3::agg3_impl<NC, 8>(tmap, a, st);
+    case 9: return v3::agg3_impl<NC, 9>(tmap, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st) {
+  switch (n) {
+    case 1: return agg3_r<1>(r, tmap, a, st); case 2: return agg3_r<2>(r, tmap, a, st);
+    case 3: return agg3_r<3>(r, tmap, a, st); case 4: return agg3_r<4>(r, tmap, a, st);
+    case 5: return agg3_r<5>(r, tmap, a, st); case 6: return agg3_r<6>(r, tmap, a, st);
+    case 7: return agg3_r<7>(r, tmap, a, st); case 8: return agg3_r<8>(r, tmap, a, st);
+    case 9: return agg3_r<9>(r, tmap, a, st);
     default: return cudaErrorInvalidValue;
   }
 }

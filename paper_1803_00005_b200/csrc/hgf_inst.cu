@@ -17,3 +17,26 @@ template cudaError_t agg2_impl<HGF_N>(const AggArgs&, cudaStream_t);
 }  // namespace v2
 #endif
 }  // namespace hgf
+
+#include "hgf_agg_v3.cuh"
+#if HGF_N <= 9
+namespace hgf {
+namespace v3 {
+template cudaError_t agg3_impl<HGF_N, 1>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 2>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 3>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 4>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 5>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 6>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 7>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 8>(const void*, const AggArgs&, cudaStream_t);
+template cudaError_t agg3_impl<HGF_N, 9>(const void*, const AggArgs&, cudaStream_t);
+}  // namespace v3
+#if HGF_N == 1
+void agg3_box(int R, int* bx, int* by) {
+  *bx = v3::box_pitch(v3::TX + 2 * R);
+  *by = v3::TY + 2 * R;
+}
+#endif
+}  // namespace hgf
+#endif

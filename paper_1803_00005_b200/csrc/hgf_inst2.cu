@@ -7,7 +7,7 @@
 
 namespace hgf {
 namespace v2 {
-template cudaError_t coef2_impl<HGF_M, HGF_D>(const float*, const float*, const float*, float*, int, int, int, int,
+template cudaError_t coef2_impl<HGF_M, HGF_D>(const float*, const float*, const float*, float*, WLayout, int, int, int, int,
                                               float, cudaStream_t);
 }  // namespace v2
 }  // namespace hgf

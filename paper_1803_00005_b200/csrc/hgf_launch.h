@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "hgf_common.cuh"
+
 namespace hgf {
 
 struct AggArgs {
@@ -43,13 +45,25 @@ namespace hgf {
 namespace v2 {
 // Fast path (n_guide <= 3, degree <= 3, radius <= 9): hgf_slice_v2.cuh, instantiated by hgf_inst.cu / hgf_inst2.cu.
 template <int M, int D>
-cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, int W, int H, int r,
+cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H, int r,
                        int L, float lam0, cudaStream_t st);
 template <int NC>
 cudaError_t agg2_impl(const AggArgs& a, cudaStream_t st);
 }  // namespace v2
 bool fast_path_ok(int m, int d, int r);
-cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf,
+cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo,
                              int W, int H, int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st);
+}  // namespace hgf
+
+namespace hgf {
+namespace v3 {
+// TMA-fed aggregation (hgf_agg_v3.cuh), n <= 9, R <= 9, W % 4 == 0; tmap points to a CUtensorMap over
+// the coefficient buffer (dims W, H, planes; box = agg3_box(n, R)).
+template <int NC, int R>
+cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st);
+}  // namespace v3
+// Box of the v3 aggregation TMA for radius R: {BX, BY} (x extent, y extent); z extent = n + 1.
+void agg3_box(int R, int* bx, int* by);
+cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
 }  // namespace hgf

@@ -49,7 +49,7 @@ __host__ __device__ inline size_t coef2_smem_floats(int M, int D, int r) {
 template <int M, int D>
 __global__ void __launch_bounds__(CoefCfg<M, D>::THREADS)
     k_coef2(const float* __restrict__ guide, const float* __restrict__ stats, const float* __restrict__ vol,
-            float* __restrict__ wbuf, int W, int H, int r, int L, float lam0) {
+            float* __restrict__ wbuf, WLayout wo, int W, int H, int r, int L, float lam0) {
   using C = CoefCfg<M, D>;
   constexpr int NC = C::NC, K = C::K, NP = C::NP, NS = C::NS, PPT = C::PPT, T = C::THREADS;
   extern __shared__ __align__(16) float sm[];
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(CoefCfg<M, D>::THREADS)
 #pragma unroll
       for (int i = 0; i < NC; ++i) c[i] = fmaf(-st[j][NP + i], S[0], S[i + 1]);
       float w0 = kap[j] * S[0];
-      float* wl = wbuf + (long long)l * K * HW + opix[j];
+      float* wl = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)(y0 + oy) * wo.pitch + (x0 + ox);
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
         float acc = 0.0f;
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(CoefCfg<M, D>::THREADS)
           acc = fmaf(st[j][a * NC - a * (a - 1) / 2 + (b - a)], c[q], acc);
         }
         w0 = fmaf(-st[j][NP + i], acc, w0);
-        wl[(i + 1) * HW] = acc;
+        wl[(i + 1) * wo.plane] = acc;
       }
       wl[0] = w0;
     }
@@ -329,14 +329,14 @@ __global__ void __launch_bounds__(B_THREADS, 1)
 }
 
 template <int M, int D>
-cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, int W, int H, int r,
+cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H, int r,
                        int L, float lam0, cudaStream_t st) {
   using C = CoefCfg<M, D>;
   const size_t smem = sizeof(float) * coef2_smem_floats(M, D, r);
   cudaError_t e = cudaFuncSetAttribute(k_coef2<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((W + A_TX - 1) / A_TX, (H + A_TY - 1) / A_TY);
-  k_coef2<M, D><<<grid, C::THREADS, smem, st>>>(guide, stats, vol, wbuf, W, H, r, L, lam0);
+  k_coef2<M, D><<<grid, C::THREADS, smem, st>>>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0);
   return cudaGetLastError();
 }
 
