@@ -6,11 +6,10 @@
 // Data movement (the binding resource is the SM's ~128 B/clk shared-memory data path, measured in
 // profiles/r01_microbench2.txt):
 //   * one cp.async.bulk.tensor (TMA) per slice brings the K = n+1 planes of w for the tile plus an
-//     R halo into SMEM.  The coefficient buffer carries a zero margin of R rows/columns above and to
-//     the left of the image (WLayout "padded"), so the tile window starting at (x0-R, y0-R) is fetched
-//     at TMA coordinate (x0, y0) >= 0 (negative TMA coordinates trap on this B200 stack, see
-//     tools/tma_test2.cu); TMA's zero fill beyond the right/bottom edge and the zero margin together
-//     implement the clipped windows (F6);
+//     R halo into SMEM (coefficient buffer rows pitched to 16 bytes).  TMA's out-of-bounds zero fill on
+//     all four sides implements the clipped windows (F6).  The tile grid is shifted so that every
+//     TMA x coordinate is 16-byte aligned: unaligned x offsets trap on this B200 stack
+//     (tools/tma_test2.cu);
 //     the next slice's TMA is issued before this slice's passes (double buffer, mbarrier-tracked);
 //   * vertical pass in place: each (plane, column) item loads its column into registers once and
 //     writes the 2R+1-row window sums back over the first TY rows;
@@ -75,7 +74,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 
 template <int NC, int R>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_agg3(const __grid_constant__ CUtensorMap tmw, const float* __restrict__ G, int W, int H, int L, int label_base,
+    k_agg3(const __grid_constant__ CUtensorMap tmw, const float* __restrict__ G, int W, int H, int pad, int L, int label_base,
            float* __restrict__ filtered_out, int do_wta, int first, int last, float* __restrict__ best_cost,
            int32_t* __restrict__ best_label, int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out,
            int64_t* __restrict__ keys_out) {
@@ -87,7 +86,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(128) float buf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(buf + NBUF * Gm::BUF_STRIDE);
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  // Tiles start at x0 = 64*bx - XSHIFT so that the TMA x coordinate x0 - R is a multiple of 4 (16 bytes):
+  // TMA traps on x offsets that are not 16-byte aligned (tools/tma_test2.cu); negative coordinates and
+  // the out-of-bounds zero fill are fine, and implement the clipped windows.
+  constexpr int XSHIFT = (4 - R % 4) % 4;
+  const int x0 = blockIdx.x * TX - XSHIFT, y0 = blockIdx.y * TY;
+  const int tx0 = x0 - R + pad, ty0 = y0 - R + pad;   // pad = 0 in the pitched layout
   const long long HW = (long long)H * W;
 
   if (tid == 0) {
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (tid == 0 && L > 0) {
     mbar_expect_tx(&bar[0], BYTES);
-    tma_load_3d(buf, &tmw, x0, y0, 0, &bar[0]);
+    tma_load_3d(buf, &tmw, tx0, ty0, 0, &bar[0]);
   }
 
   // owner role: row oy, pixels x0 + 8*seg + [0, 8)
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
   for (int j = 0; j < KX; ++j) {
     const int gx = x0 + seg * KX + j;
-    const bool in = is_owner && gy < H && gx < W;
+    const bool in = is_owner && gy < H && gx >= 0 && gx < W;
     const long long p = in ? (long long)gy * W + gx : 0;
 #pragma unroll
     for (int k = 0; k < NC; ++k) g[k][j] = in ? __ldg(G + k * HW + p) : 0.0f;
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (NBUF == 2 && tid == 0 && l + 1 < L) {           // prefetch the next slice into the other buffer
       fence_proxy_async();
       mbar_expect_tx(&bar[b ^ 1], BYTES);
-      tma_load_3d(buf + (b ^ 1) * Gm::BUF_STRIDE, &tmw, x0, y0, (l + 1) * K, &bar[b ^ 1]);
+      tma_load_3d(buf + (b ^ 1) * Gm::BUF_STRIDE, &tmw, tx0, ty0, (l + 1) * K, &bar[b ^ 1]);
     }
     // ---- vertical window sums, in place: rows [0, TY) <- sum of rows [y, y + 2R]
     for (int item = tid; item < K * Gm::WX; item += THREADS) {
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int s = 0; s < KX; ++s) {
         const int gx = x0 + seg * KX + s;
-        if (gy < H && gx < W) {
+        if (gy < H && gx >= 0 && gx < W) {
           const float zz = z[s] * invN[s];
           if (filtered_out) filtered_out[(long long)l * HW + (long long)gy * W + gx] = zz;
           if (zz < best[s]) {
@@ -193,14 +197,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (NBUF == 1 && tid == 0 && l + 1 < L) {
       fence_proxy_async();
       mbar_expect_tx(&bar[0], BYTES);
-      tma_load_3d(buf, &tmw, x0, y0, (l + 1) * K, &bar[0]);
+      tma_load_3d(buf, &tmw, tx0, ty0, (l + 1) * K, &bar[0]);
     }
   }
   if (!do_wta || !is_owner) return;
 #pragma unroll
   for (int s = 0; s < KX; ++s) {
     const int gx = x0 + seg * KX + s;
-    if (gy >= H || gx >= W) continue;
+    if (gy >= H || gx < 0 || gx >= W) continue;
     const long long p = (long long)gy * W + gx;
     if (last) {
       if (labels_out) labels_out[p] = bl[s];
@@ -224,8 +228,8 @@ cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st) {
   const size_t smem = agg3_smem_bytes<NC, R>();
   cudaError_t e = cudaFuncSetAttribute(k_agg3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.W + TX - 1) / TX, (a.H + TY - 1) / TY);
-  k_agg3<NC, R><<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.L,
+  dim3 grid((a.W + (4 - R % 4) % 4 + TX - 1) / TX, (a.H + TY - 1) / TY);
+  k_agg3<NC, R><<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.pad, a.L,
                                              a.label_base, a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
                                              a.best_label, a.labels_out, a.min_cost_out, a.keys_out);
   return cudaGetLastError();

@@ -36,7 +36,8 @@ struct hgf_ctx {
   bool fast = false;           // v2 fast-path kernels usable for (m, d, r)
   bool v3agg = false;          // TMA-fed v3 aggregation usable (n <= 9, r <= 9, W % 4 == 0)
   CUtensorMap tm_w;            // TMA descriptor over wbuf (padded layout), box agg3_box(r) x (n+1)
-  hgf::WLayout wlay{};         // coefficient-buffer layout (zero top/left margin of r when v3agg)
+  hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
+  bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
   std::string err;
   // tracing (hgf_set_profiling / hgf_profile_read)
   bool profiling = false;
@@ -85,11 +86,18 @@ cudaError_t traced(hgf_ctx* h, int cls, cudaStream_t st, F&& f) {
   return e;
 }
 
+// Coefficient-buffer budget: HGF_COEF_BUDGET_MB, else min(16 GiB, 40% of the free device memory).  The
+// v3 coefficient kernel processes labels in batches of 32, so large frames want >= 32 labels per chunk.
 size_t coef_budget_bytes() {
   const char* s = std::getenv("HGF_COEF_BUDGET_MB");
-  long long mb = s ? std::atoll(s) : 2048;
-  if (mb < 1) mb = 1;
-  return (size_t)mb << 20;
+  if (s) {
+    long long mb = std::atoll(s);
+    return (size_t)(mb < 1 ? 1 : mb) << 20;
+  }
+  size_t fr = 0, tot = 0;
+  size_t budget = (size_t)16 << 30;
+  if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr / 10 * 4 < budget) budget = fr / 10 * 4;
+  return budget < ((size_t)64 << 20) ? ((size_t)64 << 20) : budget;
 }
 
 void release(hgf_ctx* h) {
@@ -140,6 +148,9 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
 cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
+    if (h->v3coef)
+      return hgf::launch_coef_v3(h->n, h->G, h->stats, vol_chunk, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
+                                 h->stream);
     if (h->fast)
       return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                    h->stream);
@@ -165,9 +176,7 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   int bx = 0, by = 0;
   hgf::agg3_box(h->r, &bx, &by);
-  // padded layout: the image occupies rows/cols [r, r+H) x [r, r+W); the margin is zero, so a tile whose
-  // window starts at (x0 - r, y0 - r) is fetched at the non-negative TMA coordinate (x0, y0).
-  const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->r), (cuuint64_t)(h->H + h->r),
+  const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
                               (cuuint64_t)h->lcap * (h->n + 1)};
   const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
   const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)(h->n + 1)};
@@ -189,7 +198,7 @@ hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int l
     hgf::AggArgs a{};
     a.G = h->G;
     a.wbuf = h->wbuf;
-    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc;
+    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = h->wlay.pad;
     a.label_base = label_offset + c0;
     a.filtered_out = filtered_out ? filtered_out + (long long)c0 * HW : nullptr;
     a.do_wta = do_wta;
@@ -247,12 +256,13 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     const char* g = std::getenv("HGF_NO_V3");
     h->v3agg = h->fast && h->n <= 9 && !(g && g[0] == '1');     // confirmed below once the TMA map exists
   }
-  // coefficient buffer layout: padded (zero margin of r rows/cols above/left) for the TMA path
-  const hgf::WLayout flat{0, (long long)HW, W};
+  // coefficient buffer layout: rows pitched to a multiple of 4 floats for the TMA path
+  const hgf::WLayout flat{0, (long long)HW, W, 0};
   hgf::WLayout padded{};
-  padded.pitch = (W + h->r + 3) / 4 * 4;
-  padded.plane = (long long)(H + h->r) * padded.pitch;
-  padded.origin = (long long)h->r * padded.pitch + h->r;
+  padded.pad = 0;
+  padded.pitch = (W + 3) / 4 * 4;       // 16-byte rows: TMA global strides and the 128-bit stores of k_coef3
+  padded.plane = (long long)H * padded.pitch;
+  padded.origin = 0;
   h->wlay = h->v3agg ? padded : flat;
   const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
   size_t cap = coef_budget_bytes() / per_label;
@@ -272,6 +282,10 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   if (h->v3agg && !((long long)h->lcap * K <= (1LL << 31) && make_wbuf_tensor_map(h))) {
     h->v3agg = false;   // no TMA descriptor: the v2 aggregation reads the flat layout (fits the allocation)
     h->wlay = flat;
+  }
+  {
+    const char* f = std::getenv("HGF_COEF3");   // opt-in until it beats k_coef2 (profiles/r01_*)
+    h->v3coef = h->v3agg && h->n <= 6 && (f && f[0] == '1');
   }
   *out = h;
   return HGF_OK;
@@ -391,6 +405,7 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
     a.G = h->G; a.wbuf = h->wbuf; a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.label_base = l0;
+    a.pad = h->wlay.pad;
     a.filtered_out = nullptr; a.do_wta = 1; a.first = (c == 0); a.last = (c == nchunks - 1);
     a.best_cost = h->best_cost; a.best_label = h->best_label; a.labels_out = h->st_labels;
     a.min_cost_out = nullptr; a.keys_out = nullptr;

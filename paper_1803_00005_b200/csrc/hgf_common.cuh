@@ -35,9 +35,10 @@ __device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
 // origin + (l*(n+1) + k)*plane + y*pitch + x.  The v3 aggregation pads it with a zero top/left margin
 // (TMA tiles are then fetched at non-negative coordinates).
 struct WLayout {
-  long long origin;
+  long long origin;   // = pad * pitch + pad
   long long plane;
-  int pitch;
+  int pitch;          // multiple of 4 in the padded layout (16-byte rows)
+  int pad;            // zero margin above / left of the image (0 = flat layout; else roundup(r, 4))
 };
 
 // Number of statistics planes stored per pixel for n channels: P' (upper triangle) + nu.

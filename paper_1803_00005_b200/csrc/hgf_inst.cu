@@ -19,6 +19,15 @@ template cudaError_t agg2_impl<HGF_N>(const AggArgs&, cudaStream_t);
 }  // namespace hgf
 
 #include "hgf_agg_v3.cuh"
+#include "hgf_coef_v3.cuh"
+#if HGF_N <= 6
+namespace hgf {
+namespace v3 {
+template cudaError_t coef3_impl<HGF_N>(const float*, const float*, const float*, float*, WLayout, int, int, int, int,
+                                       float, cudaStream_t);
+}  // namespace v3
+}  // namespace hgf
+#endif
 #if HGF_N <= 9
 namespace hgf {
 namespace v3 {

@@ -11,6 +11,7 @@ struct AggArgs {
   const float* G;
   const float* wbuf;
   int W, H, r, L, label_base;
+  int pad;   // zero margin of the coefficient layout (v3 aggregation)
   float* filtered_out;
   int do_wta, first, last;
   float* best_cost;
@@ -66,4 +67,12 @@ cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st);
 // Box of the v3 aggregation TMA for radius R: {BX, BY} (x extent, y extent); z extent = n + 1.
 void agg3_box(int R, int* bx, int* by);
 cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
+namespace v3 {
+template <int NC>
+cudaError_t coef3_impl(const float* G, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H,
+                       int r, int L, float lam0, cudaStream_t st);
+}  // namespace v3
+// Label-batched marching coefficient kernel (hgf_coef_v3.cuh): n <= 6, r <= 9, padded layout.
+cudaError_t launch_coef_v3(int n, const float* G, const float* stats, const float* vol, float* wbuf, WLayout wo,
+                           int W, int H, int r, int L, float lam0, cudaStream_t st);
 }  // namespace hgf
