@@ -166,3 +166,18 @@ def test_invalid_arguments_fail_loudly():
     h = HGF(10, 10, 3, 2, 2, 0.05)
     with pytest.raises(HGFError):
         h.aggregate_wta(torch.zeros(3, 10, 10, device="cuda"), torch.zeros(2, 10, 11, device="cuda"))
+
+
+@pytest.mark.parametrize("kernel_env", ["HGF_COEF3", "HGF_NO_V3", "HGF_FORCE_V1"])
+def test_kernel_variants_parity(monkeypatch, kernel_env):
+    """Every coefficient/aggregation kernel variant against the oracle (k_coef3, v2 flat layout, v1)."""
+    monkeypatch.setenv(kernel_env, "1")
+    c = synth.config("C2")
+    scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
+    V = synth.stereo_cost_volume_np(scene, 40)[:, :200, :260].copy()
+    I = np.ascontiguousarray(scene.left[:, :200, :260])
+    res = _run(I, V, c["d"], c["r"], c["lam"])
+    Z = O.hgf_filter(I, V, c["lam"], c["r"], c["d"])
+    s_v = float(np.abs(V).max())
+    check_z(res["filtered"], Z, s_v)
+    check_labels(res["labels"], Z, s_v)
