@@ -49,3 +49,10 @@ void agg3_box(int R, int* bx, int* by) {
 #endif
 }  // namespace hgf
 #endif
+
+#include "hgf_stats_v2.cuh"
+namespace hgf {
+namespace st2 {
+template cudaError_t stats2_impl<HGF_N>(const float*, float*, int, int, int, double, int, cudaStream_t);
+}  // namespace st2
+}  // namespace hgf

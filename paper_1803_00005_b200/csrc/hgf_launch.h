@@ -76,3 +76,10 @@ cudaError_t coef3_impl(const float* G, const float* stats, const float* vol, flo
 cudaError_t launch_coef_v3(int n, const float* G, const float* stats, const float* vol, float* wbuf, WLayout wo,
                            int W, int H, int r, int L, float lam0, cudaStream_t st);
 }  // namespace hgf
+
+namespace hgf {
+namespace st2 {
+template <int NC>
+cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st);
+}  // namespace st2
+}  // namespace hgf

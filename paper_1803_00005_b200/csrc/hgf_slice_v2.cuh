@@ -46,10 +46,12 @@ __host__ __device__ inline size_t coef2_smem_floats(int M, int D, int r) {
   return (size_t)M * IY * IX + 2 * (size_t)IY * IX + (size_t)K * IY * (A_TX + 1) + (size_t)K * A_TY * A_TX;
 }
 
-template <int M, int D>
+// R > 0: compile-time radius (tile geometry and every window offset fold into immediates); R = 0: runtime r.
+template <int M, int D, int R>
 __global__ void __launch_bounds__(CoefCfg<M, D>::THREADS)
     k_coef2(const float* __restrict__ guide, const float* __restrict__ stats, const float* __restrict__ vol,
-            float* __restrict__ wbuf, WLayout wo, int W, int H, int r, int L, float lam0) {
+            float* __restrict__ wbuf, WLayout wo, int W, int H, int r_arg, int L, float lam0) {
+  const int r = (R > 0) ? R : r_arg;
   using C = CoefCfg<M, D>;
   constexpr int NC = C::NC, K = C::K, NP = C::NP, NS = C::NS, PPT = C::PPT, T = C::THREADS;
   extern __shared__ __align__(16) float sm[];
@@ -328,16 +330,28 @@ __global__ void __launch_bounds__(B_THREADS, 1)
   }
 }
 
-template <int M, int D>
-cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H, int r,
+template <int M, int D, int R>
+cudaError_t coef2_r(const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H, int r,
                        int L, float lam0, cudaStream_t st) {
   using C = CoefCfg<M, D>;
   const size_t smem = sizeof(float) * coef2_smem_floats(M, D, r);
-  cudaError_t e = cudaFuncSetAttribute(k_coef2<M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_coef2<M, D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((W + A_TX - 1) / A_TX, (H + A_TY - 1) / A_TY);
-  k_coef2<M, D><<<grid, C::THREADS, smem, st>>>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0);
+  k_coef2<M, D, R><<<grid, C::THREADS, smem, st>>>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0);
   return cudaGetLastError();
+}
+
+template <int M, int D>
+cudaError_t coef2_impl(const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H,
+                       int r, int L, float lam0, cudaStream_t st) {
+  switch (r) {   // the BASELINE radii get compile-time kernels; others use the runtime-r instance
+    case 2: return coef2_r<M, D, 2>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st);
+    case 4: return coef2_r<M, D, 4>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st);
+    case 7: return coef2_r<M, D, 7>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st);
+    case 9: return coef2_r<M, D, 9>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st);
+    default: return coef2_r<M, D, 0>(guide, stats, vol, wbuf, wo, W, H, r, L, lam0, st);
+  }
 }
 
 template <int NC>

@@ -1,0 +1,170 @@
+// Label-independent statistics, version 2 (k_stats2<n>): float64 Gram planes by sliding-window sums.
+//
+//   G_ij = B(G_i G_j), 0 <= i <= j <= n, G_0 = ones inside the image (Prop 2; Eq12),
+//   then per pixel the Prop-1 recursion (Eq4 P:143-151 with readings F1/F2, as in k_stats) giving
+//   P' = -lambda alpha_{1..n,1..n} and nu = B(G_k)/(lambda_0 + N), stored as float32 planes.
+//
+// All n+1 channel tiles (16x16 outputs + r halo, float32) are staged in SMEM once; the product planes
+// are box-filtered 8 pairs at a time: horizontal sliding sums (one thread per (pair, row), float64)
+// then vertical sliding sums (one thread per (pair, column)), so each product costs O(1) adds per
+// output instead of the 2r+1 taps of k_stats.  fp32 x fp32 products are exact in float64.
+#pragma once
+#include "hgf_common.cuh"
+#include "hgf_launch.h"
+
+namespace hgf {
+namespace st2 {
+
+constexpr int T = 16;        // output tile side
+constexpr int PB = 8;        // product planes per batch
+constexpr int THREADS = T * T;
+
+__host__ __device__ inline size_t smem_bytes(int NC, int r) {
+  const int TS = T + 2 * r;
+  return (size_t)(NC + 1) * TS * TS * 4 + (size_t)PB * TS * T * 8 + (size_t)PB * T * T * 8 + 16;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G, float* __restrict__ stats, int W,
+                                                    int H, int r, double lam, int mode) {
+  constexpr int K = NC + 1;
+  constexpr int NPAIR = K * (K + 1) / 2 - 1;     // (0,0) is N_p, analytic
+  constexpr int NB = (NPAIR + PB - 1) / PB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int TS = T + 2 * r;
+  float* tiles = reinterpret_cast<float*>(smem_raw);                              // [K][TS][TS]
+  double* hb = reinterpret_cast<double*>(smem_raw + (((size_t)K * TS * TS * 4 + 15) & ~(size_t)15));  // [PB][TS][T]
+  double* vb = hb + PB * TS * T;                                                  // [PB][T][T]
+  const int tid = threadIdx.x;
+  const int tx = tid % T, ty = tid / T;
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
+  const long long HW = (long long)H * W;
+
+  for (int e = tid; e < K * TS * TS; e += THREADS) {
+    const int c = e / (TS * TS), rem = e % (TS * TS);
+    const int yy = y0 - r + rem / TS, xx = x0 - r + rem % TS;
+    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
+    tiles[e] = in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)yy * W + xx)) : 0.0f;
+  }
+
+  double g[NPAIR];
+#pragma unroll
+  for (int bt = 0; bt < NB; ++bt) {
+    __syncthreads();   // tiles ready (first batch) / vb consumed (later batches)
+    // horizontal sliding sums of the products of this batch's pairs
+    for (int item = tid; item < PB * TS; item += THREADS) {
+      const int pb = item / TS, row = item % TS;
+      const int p = bt * PB + pb;
+      if (p >= NPAIR) continue;
+      // pair index p -> (i, j), i <= j, enumerated row-major over the upper triangle, skipping (0,0)
+      int i = 0, q = p + 1;
+      while (q >= K - i) { q -= K - i; ++i; }
+      const int j = i + q;
+      const float* ti = tiles + (i * TS + row) * TS;
+      const float* tj = tiles + (j * TS + row) * TS;
+      double acc = 0.0;
+      for (int dx = 0; dx <= 2 * r; ++dx) acc += (double)ti[dx] * (double)tj[dx];
+      double* ho = hb + (pb * TS + row) * T;
+      ho[0] = acc;
+#pragma unroll
+      for (int c = 1; c < T; ++c) {
+        acc += (double)ti[c + 2 * r] * (double)tj[c + 2 * r] - (double)ti[c - 1] * (double)tj[c - 1];
+        ho[c] = acc;
+      }
+    }
+    __syncthreads();
+    for (int item = tid; item < PB * T; item += THREADS) {
+      const int pb = item / T, col = item % T;
+      if (bt * PB + pb >= NPAIR) continue;
+      const double* hc = hb + pb * TS * T + col;
+      double acc = 0.0;
+      for (int dy = 0; dy <= 2 * r; ++dy) acc += hc[dy * T];
+      double* vo = vb + pb * T * T + col;
+      vo[0] = acc;
+#pragma unroll
+      for (int y = 1; y < T; ++y) {
+        acc += hc[(y + 2 * r) * T] - hc[(y - 1) * T];
+        vo[y * T] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int pb = 0; pb < PB; ++pb)
+      if (bt * PB + pb < NPAIR) g[bt * PB + pb] = vb[(pb * T + ty) * T + tx];
+  }
+  const int gx = x0 + tx, gy = y0 + ty;
+  if (gx >= W || gy >= H) return;
+  const double N = (double)window_count(gy, gx, H, W, r);
+  double Gm[K][K];
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int b = a; b < K; ++b) {
+      const int idx = a * K - a * (a - 1) / 2 + (b - a) - 1;   // position in g (pair (a,b), (0,0) removed)
+      const double v = (a == 0 && b == 0) ? N : g[idx];
+      Gm[a][b] = v;
+      Gm[b][a] = v;
+    }
+  const double inv_lam = 1.0 / lam;
+  const int c0 = (mode == 0) ? 0 : 1;
+  if (mode != 0) {
+#pragma unroll
+    for (int a = 1; a < K; ++a)
+#pragma unroll
+      for (int b = 1; b < K; ++b) Gm[a][b] = Gm[a][b] - Gm[0][a] * Gm[0][b] / N;   // centred Gram (§5.1)
+  }
+  double al[K][K];
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int b = 0; b < K; ++b) al[a][b] = 0.0;
+  al[c0][c0] = -inv_lam / (lam + Gm[c0][c0]);                              // F1
+#pragma unroll
+  for (int k = 1; k < K; ++k) {
+    if (k <= c0) continue;
+    double u[K];
+    double quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < k; ++m) s += al[i][m] * Gm[m][k];               // u_i
+      u[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < k; ++i) quad += Gm[k][i] * u[i];
+    const double gam = -1.0 / (1.0 + inv_lam * Gm[k][k] + quad);          // gamma^kappa
+#pragma unroll
+    for (int i = 0; i < k; ++i)
+#pragma unroll
+      for (int j = 0; j < k; ++j) al[i][j] += gam * u[i] * u[j];          // gamma F + alpha (F2)
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      al[i][k] = inv_lam * gam * u[i];
+      al[k][i] = al[i][k];
+    }
+    al[k][k] = inv_lam * inv_lam * gam;
+  }
+  const long long p = (long long)gy * W + gx;
+  int s = 0;
+#pragma unroll
+  for (int a = 1; a < K; ++a)
+#pragma unroll
+    for (int b = a; b < K; ++b) stats[(long long)(s++) * HW + p] = (float)(-lam * al[a][b]);
+  const double den = (mode == 0) ? (lam + N) : N;
+#pragma unroll
+  for (int a = 1; a < K; ++a) stats[(long long)(s++) * HW + p] = (float)(Gm[0][a] / den);
+}
+
+template <int NC>
+cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st) {
+  const size_t smem = smem_bytes(NC, r);
+  cudaError_t e = cudaFuncSetAttribute(k_stats2<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((W + T - 1) / T, (H + T - 1) / T);
+  k_stats2<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode);
+  return cudaGetLastError();
+}
+
+}  // namespace st2
+}  // namespace hgf
