@@ -144,13 +144,45 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
   return HGF_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library does not link libcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D float32 tensor map (x fastest), element strides 1, zero fill out of bounds, no swizzle.
+bool encode_map_3d(CUtensorMap* tm, const void* base, long long dx, long long dy, long long dz, long long pitch,
+                   long long plane, int bx, int by, int bz) {
+  auto encode = tensor_map_encoder();
+  if (!encode || ((uintptr_t)base & 15) || ((pitch * 4) & 15) || ((plane * 4) & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)dx, (cuuint64_t)dy, (cuuint64_t)dz};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // K4a for one chunk of Lc slices: the v2 fast path when (m, d, r) allow it, else the generic v1 kernel.
 cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
-    if (h->v3coef)
-      return hgf::launch_coef_v3(h->n, h->G, h->stats, vol_chunk, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
+    if (h->v3coef) {
+      // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 88 x 1 x 32 (k_coef3)
+      CUtensorMap tm_vol;
+      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, 88, 1, 32))
+        return cudaErrorInvalidValue;
+      return hgf::launch_coef_v3(h->n, &tm_vol, h->G, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                  h->stream);
+    }
     if (h->fast)
       return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                    h->stream);
@@ -285,7 +317,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   }
   {
     const char* f = std::getenv("HGF_COEF3");   // opt-in until it beats k_coef2 (profiles/r01_*)
-    h->v3coef = h->v3agg && h->n <= 6 && (f && f[0] == '1');
+    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && (f && f[0] == '1');
   }
   *out = h;
   return HGF_OK;

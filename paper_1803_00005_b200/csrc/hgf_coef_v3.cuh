@@ -1,23 +1,28 @@
-// HGF per-slice coefficients, version 3 (k_coef3<n>): label-batched row marching, warp-specialised.
+// HGF per-slice coefficients, version 3 (k_coef3<n, R>): label-batched row marching, warp-specialised,
+// TMA-fed.
 //
 // For each slice l and pixel p (Eq12 with G_{n+1} = p; Eq13 P:304 reassociated):
 //     S_0 = B(p),  S_k = B(G_k p)  (k = 1..n),   w = P'(S - nu S_0),   w_0 = S_0/(lambda_0 + N) - nu^T w
 //
-// A CTA owns a strip of TX = 64 columns x a band of BH rows x a batch of LB = 32 labels, and marches
-// down the band one row at a time:
-//   * V warps (producers): thread = (column c of the strip plus an r halo, group of 8 labels).  It keeps
-//     the vertical running sums V_k(c) = sum_{|dy|<=r} G_k p over the window for its 8 labels in registers
-//     (7 x 8 values at n = 6), adding the entering row and subtracting the leaving row (both read straight
-//     from global memory: coalesced across columns; the leaving row is an L2 hit).  G_k is label-invariant
-//     and is loaded once per row for all 8 labels.  The row of V for the 32 labels goes to SMEM.
-//   * H warps (consumers): thread = (label, 16-pixel segment).  It slides the horizontal 2r+1 window over
-//     the row of V (S for one pixel at a time, all planes), reads that pixel's statistics from SMEM (the
-//     same address for 16 lanes: a broadcast, so the 27 floats per pixel cost ~1 word per voxel), does the
-//     n x n matvec and stores w 8 pixels at a time (32-byte runs).
-//   * V and H warps run one row apart through a double-buffered SMEM row (named barriers FULL/FREE).
-// Label-invariant data (G, statistics) thus never costs per-label shared-memory traffic, which was the
-// dominant cost of the tile version (profiles/r01_ncu_v2_coef2_sass_mix.txt).
+// A CTA owns a strip of TX = 64 columns x a band of BH rows x a batch of LB = 32 labels and marches down
+// the band one image row per step:
+//   * TMA (one elected V thread): per step, the entering row (y+R) and the leaving row (y-R-1) of the
+//     32 labels' cost slices and of the n guidance planes land in SMEM (2-stage ring, mbarrier-tracked,
+//     issued two steps ahead).  Rows/labels/columns outside the image read as zero (clipped windows).
+//   * V warps (producers): thread = (column c of the strip plus an R halo, group of 8 labels); it keeps the
+//     vertical running sums V_k(c) = sum_{|dy|<=R} G_k p of its 8 labels in registers, and per output row
+//     writes the V row of the 32 labels, plus the row's statistics (27 floats + 1/(lambda_0+N) per pixel,
+//     array-of-structs) to SMEM.
+//   * H warps (consumers): thread = (label, 8-pixel segment); slides the horizontal 2R+1 window over the V
+//     row, reads each pixel's statistics with 128-bit loads shared by 16 lanes (a broadcast), does the
+//     n x n matvec and stores w as 16-byte runs.
+//   * V and H warps run one row apart through a double-buffered SMEM V row (named barriers FULL/FREE).
+// Label-invariant data (G, statistics) never costs per-label shared-memory traffic.
 #pragma once
+#include <cuda.h>
+
+#include <cuda/ptx>
+
 #include "hgf_common.cuh"
 #include "hgf_launch.h"
 
@@ -28,90 +33,165 @@ constexpr int C_TX = 64;                    // owned columns per strip
 constexpr int C_LB = 32;                    // labels per CTA batch
 constexpr int C_LG = 8;                     // labels per V thread
 constexpr int C_NG = C_LB / C_LG;           // V label groups
-constexpr int C_HSEG = 16;                  // pixels per H thread
-constexpr int C_NHW = 4;                    // H warps: 16 labels x 2 segments each
+constexpr int C_HSEG = 8;                   // pixels per H thread
+constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
+constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = 16 labels x 2 segments
 constexpr int C_RMAX = 9;
+constexpr int C_BXP = 88;                   // TMA box width: >= TX + 2*RMAX + 3 (x start rounded down to 16 B)
+constexpr int C_SPX = 28;                   // floats per pixel in the SMEM statistics row (27 + kappa)
+constexpr int C_SSEG = C_HSEG * C_SPX + 16; // segment stride: consecutive segments 16 banks apart
+constexpr int C_BAR_V = 5;                  // named barrier among the V warps
 
 template <int NC>
 struct CoefGeom {
   static constexpr int K = NC + 1, NP = NC * (NC + 1) / 2, NS = NP + NC;
+  static_assert(NS + 1 <= C_SPX, "statistics + kappa must fit the per-pixel slot");
   static constexpr int CXMAX = C_TX + 2 * C_RMAX;         // V columns (strip + halo), max 82
   static constexpr int CP = CXMAX | 1;                      // SMEM column pitch (odd)
-  static constexpr int LSTRIDE = K * CP + ((K * CP) % 2 == 0 ? 1 : 0);  // floats per label: odd -> the
-                                                            // 16 labels x 2 segments of an H warp hit 32 banks
+  static constexpr int LSTRIDE = K * CP + ((K * CP) % 2 == 0 ? 1 : 0);  // floats per label (odd)
   static constexpr int VROW = C_LB * LSTRIDE;               // floats per V row buffer
-  static constexpr int SROW = NS * C_TX;                    // statistics row [NS][64]
+  static constexpr int SROW = C_NSEG * C_SSEG;              // statistics row
+  // one TMA stage: entering + leaving rows of the 32 labels' cost slices (128-byte aligned sizes)
+  static constexpr int PROW = C_LB * C_BXP;
+  static constexpr int STAGE = 2 * PROW;
+  // per (segment, label): the 2R+1 window sums of the segment's first pixel, computed by the V warps
+  static constexpr int ISEG = C_LB * K + 16 + ((C_LB * K) % 32 == 16 ? 16 : 0);  // = 16 banks mod 32
+  static constexpr int INI = C_NSEG * ISEG;
   static constexpr int NVW = (CXMAX * C_NG + 31) / 32;      // V warps
   static constexpr int THREADS = (NVW + C_NHW) * 32;
-  static constexpr size_t SMEM = sizeof(float) * (2 * (size_t)VROW + 2 * (size_t)SROW);
+  static constexpr size_t SMEM =
+      sizeof(float) * (2 * (size_t)STAGE + 2 * (size_t)VROW + 2 * (size_t)SROW + 2 * (size_t)INI) + 64;
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void c3_tma_3d(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+  const int32_t c[3] = {x, y, z};
+  cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, dst, tm, c, bar);
+}
 
-template <int NC>
+// R > 0: compile-time radius; R == 0: runtime radius r_arg (<= C_RMAX).
+template <int NC, int R>
 __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
-    k_coef3(const float* __restrict__ G, const float* __restrict__ stats, const float* __restrict__ vol,
-            float* __restrict__ wbuf, WLayout wo, int W, int H, int r, int L, int BH, float lam0) {
+    k_coef3(const __grid_constant__ CUtensorMap tm_vol, const float* __restrict__ G,
+            const float* __restrict__ stats, float* __restrict__ wbuf, WLayout wo, int W, int H, int r_arg, int L,
+            int BH, float lam0) {
   using Gm = CoefGeom<NC>;
   constexpr int K = Gm::K, NP = Gm::NP, NS = Gm::NS, CP = Gm::CP, LSTRIDE = Gm::LSTRIDE;
   constexpr int NV = Gm::NVW * 32, NH = C_NHW * 32, NALL = NV + NH;
-  extern __shared__ __align__(16) float sm[];
-  float* vrow = sm;                       // [2][LB][K][CP]
-  float* srow = sm + 2 * Gm::VROW;        // [2][NS][TX]
+  const int r = (R > 0) ? R : r_arg;
+  extern __shared__ __align__(128) float sm[];
+  float* stage = sm;                              // [2][STAGE]: pe[32][BXP], pl[32][BXP], ge[NC][BXP], gl[NC][BXP]
+  float* vrow = sm + 2 * Gm::STAGE;               // [2][LB][K][CP]
+  float* srow = vrow + 2 * Gm::VROW;              // [2][NSEG][HSEG][SPX] (+16 pad per segment)
+  float* ini = srow + 2 * Gm::SROW;               // [2][NSEG][ISEG]: [label][K] window sums per segment
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ini + 2 * Gm::INI);
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * C_TX;
   const int Y0 = blockIdx.y * BH, Y1 = min(H, Y0 + BH);
   const int lb0 = blockIdx.z * C_LB;
   const long long HW = (long long)H * W;
-  const int CX = C_TX + 2 * r;            // V columns used: image x = x0 - r + c
+  const int CX = C_TX + 2 * r;                    // V columns used: image x = x0 - r + c
+  const int xt = ((x0 - r) >> 2) << 2;            // TMA x start (16-byte aligned; arithmetic shift floors)
+  const int sh = (x0 - r) - xt;                   // SMEM column of V column 0
+  const int nsteps = 2 * r + (Y1 - Y0);           // entering rows Y0-r .. Y1-1+r
 
   if (tid < NV) {
     // ============================ V warps (producers) ============================
     const int g = tid / CX, c = tid % CX;
     const bool active = g < C_NG;
-    const int xx = x0 - r + c;
-    const bool xin = active && xx >= 0 && xx < W;
-    int nl = 0;                            // labels of this thread inside [0, L)
-    const float* pv[C_LG];
+    const int cs = c + sh;
+    if (tid == 0) {
+      cuda::ptx::mbarrier_init(&bar[0], 1);
+      cuda::ptx::mbarrier_init(&bar[1], 1);
+      cuda::ptx::fence_mbarrier_init(cuda::ptx::sem_release, cuda::ptx::scope_cluster);
+    }
+    named_sync(C_BAR_V, NV);
+    // step t: entering row Y0 - r + t, leaving row Y0 - 2r - 1 + t (from t = 2r + 1), output row Y0 - r + t - r
+    auto issue = [&](int t) {
+      float* s = stage + (t & 1) * Gm::STAGE;
+      const int ye = Y0 - r + t;
+      const bool leave = t >= 2 * r + 1;
+      const unsigned bytes = (unsigned)(((leave ? 2 : 1) * Gm::PROW) * 4);
+      cuda::ptx::mbarrier_arrive_expect_tx(cuda::ptx::sem_release, cuda::ptx::scope_cta, cuda::ptx::space_shared,
+                                           &bar[t & 1], bytes);
+      c3_tma_3d(s, &tm_vol, xt, ye, lb0, &bar[t & 1]);
+      if (leave) c3_tma_3d(s + Gm::PROW, &tm_vol, xt, ye - 2 * r - 1, lb0, &bar[t & 1]);
+    };
+    // guidance values of this column for the entering / leaving rows of step t (label-invariant, prefetched
+    // one step ahead in registers)
+    const int gxc = x0 - r + c;
+    const bool gin = active && gxc >= 0 && gxc < W;
+    auto load_g = [&](int t, float (&ge)[NC > 0 ? NC : 1], float (&gl)[NC > 0 ? NC : 1]) {
+      const int ye = Y0 - r + t, yl = ye - 2 * r - 1;
+      const bool ein = gin && t < nsteps && ye >= 0 && ye < H;
+      const bool lin = gin && t < nsteps && t >= 2 * r + 1 && yl >= 0 && yl < H;
 #pragma unroll
-    for (int j = 0; j < C_LG; ++j) {
-      const int l = lb0 + g * C_LG + j;
-      const bool ok = active && l < L;
-      nl += ok ? 1 : 0;
-      pv[j] = vol + (ok ? (long long)l : 0) * HW + (xin ? xx : 0);
+      for (int k = 0; k < NC; ++k) {
+        ge[k] = ein ? __ldg(G + k * HW + (long long)ye * W + gxc) : 0.0f;
+        gl[k] = lin ? __ldg(G + k * HW + (long long)yl * W + gxc) : 0.0f;
+      }
+    };
+    float gen[NC > 0 ? NC : 1], gln[NC > 0 ? NC : 1];
+    load_g(0, gen, gln);
+    if (tid == 0) {
+      issue(0);
+      if (nsteps > 1) issue(1);
     }
     float acc[C_LG][K];
 #pragma unroll
     for (int j = 0; j < C_LG; ++j)
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[j][k] = 0.0f;
-    // add (sgn = +1) or subtract (sgn = -1) image row yy's contribution
-    auto update = [&](int yy, float sgn) {
-      if (!xin || yy < 0 || yy >= H) return;
-      const long long ro = (long long)yy * W;
-      float gk[NC > 0 ? NC : 1];
+    // statistics of output row y for this thread's share of the strip (prefetched one row ahead)
+    constexpr int SPT = ((NS + 1) * C_TX + NV - 1) / NV;
+    float spre[SPT];
+    auto load_stats = [&](int y) {
 #pragma unroll
-      for (int k = 0; k < NC; ++k) gk[k] = __ldg(G + k * HW + ro + xx);
-#pragma unroll
-      for (int j = 0; j < C_LG; ++j) {
-        if (j < nl) {
-          const float p = __ldg(pv[j] + ro) * sgn;
-          acc[j][0] += p;
-#pragma unroll
-          for (int k = 0; k < NC; ++k) acc[j][k + 1] = fmaf(gk[k], p, acc[j][k + 1]);
-        }
+      for (int q = 0; q < SPT; ++q) {
+        const int e = tid + q * NV;
+        const int s = e / C_TX, x = e % C_TX, gx = x0 + x;
+        float v = 0.0f;
+        if (e < (NS + 1) * C_TX && y < Y1 && gx < W)
+          v = (s < NS) ? __ldg(stats + s * HW + (long long)y * W + gx)
+                       : 1.0f / (lam0 + (float)window_count(y, gx, H, W, r));
+        spre[q] = v;
       }
     };
-    // warm-up window of the band's first output row: rows [Y0 - r, Y0 + r - 1]
-    for (int yy = Y0 - r; yy < Y0 + r; ++yy) update(yy, 1.0f);
-    for (int y = Y0; y < Y1; ++y) {
+    load_stats(Y0);
+    for (int t = 0; t < nsteps; ++t) {
+      const float* s = stage + (t & 1) * Gm::STAGE;
+      while (!cuda::ptx::mbarrier_try_wait_parity(&bar[t & 1], (t >> 1) & 1)) {
+      }
+      const bool leave = t >= 2 * r + 1;
+      float ge[NC > 0 ? NC : 1], gl[NC > 0 ? NC : 1];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        ge[k] = gen[k];
+        gl[k] = gln[k];
+      }
+      load_g(t + 1, gen, gln);
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < C_LG; ++j) {
+          const float pe = s[(g * C_LG + j) * C_BXP + cs];
+          const float pl = leave ? s[Gm::PROW + (g * C_LG + j) * C_BXP + cs] : 0.0f;
+          acc[j][0] += pe - pl;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) acc[j][k + 1] = fmaf(ge[k], pe, fmaf(-gl[k], pl, acc[j][k + 1]));
+        }
+      }
+      named_sync(C_BAR_V, NV);                         // every V thread is done with stage t & 1
+      if (tid == 0 && t + 2 < nsteps) {
+        cuda::ptx::fence_proxy_async(cuda::ptx::space_shared);
+        issue(t + 2);
+      }
+      const int y = Y0 - r + t - r;                    // output row completed by this step
+      if (y < Y0) continue;
       const int b = (y - Y0) & 1;
-      if (y - Y0 >= 2) named_sync(3 + b, NALL);   // H warps released buffer b
-      update(y + r, 1.0f);
-      if (y > Y0) update(y - r - 1, -1.0f);
+      if (y - Y0 >= 2) named_sync(3 + b, NALL);        // H warps released buffer b
       if (active) {
         float* dst = vrow + b * Gm::VROW + (g * C_LG) * LSTRIDE + c;
 #pragma unroll
@@ -119,84 +199,97 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < K; ++k) dst[j * LSTRIDE + k * CP] = acc[j][k];
       }
-      // statistics row y for the strip's 64 owned pixels (consumed by the H warps with this V row)
       float* sdst = srow + b * Gm::SROW;
-      for (int e = tid; e < NS * C_TX; e += NV) {
-        const int s = e / C_TX, x = e % C_TX;
-        sdst[e] = (x0 + x < W) ? __ldg(stats + s * HW + (long long)y * W + x0 + x) : 0.0f;
+#pragma unroll
+      for (int q = 0; q < SPT; ++q) {
+        const int e = tid + q * NV;
+        if (e < (NS + 1) * C_TX) {
+          const int sidx = e / C_TX, x = e % C_TX;
+          sdst[(x / C_HSEG) * C_SSEG + (x % C_HSEG) * C_SPX + sidx] = spre[q];
+        }
       }
-      named_arrive(1 + b, NALL);                   // row y ready in buffer b
+      // window sums of every (segment, label, plane) at the segment's first pixel: the H warps start their
+      // sliding windows from these instead of summing 2R+1 columns each (moves ~1/4 of the H work here)
+      named_sync(C_BAR_V, NV);
+      for (int item = tid; item < C_NSEG * C_LB * K; item += NV) {
+        const int sg = item / (C_LB * K), rem = item % (C_LB * K);
+        const float* colp = vrow + b * Gm::VROW + (rem / K) * LSTRIDE + (rem % K) * CP + sg * C_HSEG;
+        float a = 0.0f;
+        if (R > 0) {
+#pragma unroll
+          for (int j = 0; j <= 2 * R; ++j) a += colp[j];
+        } else {
+          for (int j = 0; j <= 2 * r; ++j) a += colp[j];
+        }
+        ini[b * Gm::INI + sg * Gm::ISEG + rem] = a;
+      }
+      named_arrive(1 + b, NALL);                       // row y ready in buffer b
+      load_stats(y + 1);
     }
   } else {
     // ============================ H warps (consumers) ============================
     const int h = tid - NV, hw = h >> 5, ln = h & 31;
     const int lab = (hw & 1) * 16 + (ln & 15);        // label within the batch
-    const int seg = 2 * (hw >> 1) + (ln >> 4);        // 16-pixel segment 0..3
+    const int seg = 2 * (hw >> 1) + (ln >> 4);        // 8-pixel segment 0..7
     const int l = lb0 + lab;
     const bool lok = l < L;
     const int xs = seg * C_HSEG;                      // first owned pixel (strip-relative)
+    const bool full = x0 + xs + C_HSEG <= W;
     for (int y = Y0; y < Y1; ++y) {
       const int b = (y - Y0) & 1;
       named_sync(1 + b, NALL);
-      const float* vr = vrow + b * Gm::VROW + lab * LSTRIDE;
-      const float* st = srow + b * Gm::SROW;
+      const float* vr = vrow + b * Gm::VROW + lab * LSTRIDE + xs;    // V column xs of plane 0
+      const float* st = srow + b * Gm::SROW + seg * C_SSEG;
+      const float* ip = ini + b * Gm::INI + seg * Gm::ISEG + lab * K;
       float S[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        float a = 0.0f;
-        for (int j = 0; j <= 2 * r; ++j) a += vr[k * CP + xs + j];
-        S[k] = a;
-      }
-      float wv[K][8];
-      float* wrow = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)y * wo.pitch + x0 + xs;
-#pragma unroll 1
-      for (int q = 0; q < C_HSEG; q += 8) {
+      for (int k = 0; k < K; ++k) S[k] = ip[k];
+      float wv[K][C_HSEG];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int x = xs + q + i;                 // strip-relative pixel
-          if (q + i > 0) {
+      for (int i = 0; i < C_HSEG; ++i) {
+        if (i > 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) S[k] += vr[k * CP + x + 2 * r] - vr[k * CP + x - 1];
-          }
-          // statistics of pixel (y, x0 + x): P' (upper triangle) then nu  -- broadcast reads
-          float sp[NS];
-#pragma unroll
-          for (int s = 0; s < NS; ++s) sp[s] = st[s * C_TX + x];
-          const int gx = x0 + x;
-          const float kap = 1.0f / (lam0 + (float)window_count(y, gx < W ? gx : W - 1, H, W, r));
-          float cc[NC > 0 ? NC : 1];
-#pragma unroll
-          for (int k = 0; k < NC; ++k) cc[k] = fmaf(-sp[NP + k], S[0], S[k + 1]);
-          float w0 = kap * S[0];
-#pragma unroll
-          for (int a = 0; a < NC; ++a) {
-            float t = 0.0f;
-#pragma unroll
-            for (int bq = 0; bq < NC; ++bq) {
-              const int lo = a < bq ? a : bq, hi = a < bq ? bq : a;
-              t = fmaf(sp[lo * NC - lo * (lo - 1) / 2 + (hi - lo)], cc[bq], t);
-            }
-            wv[a + 1][i] = t;
-            w0 = fmaf(-sp[NP + a], t, w0);
-          }
-          wv[0][i] = w0;
+          for (int k = 0; k < K; ++k) S[k] += vr[k * CP + i + 2 * r] - vr[k * CP + i - 1];
         }
-        if (lok) {
-          const int gx0 = x0 + xs + q;
-          if (gx0 + 8 <= W) {
+        float sp[C_SPX];
+        const float4* s4 = reinterpret_cast<const float4*>(st + i * C_SPX);
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-              float4* d4 = reinterpret_cast<float4*>(wrow + k * wo.plane + q);
-              d4[0] = make_float4(wv[k][0], wv[k][1], wv[k][2], wv[k][3]);
-              d4[1] = make_float4(wv[k][4], wv[k][5], wv[k][6], wv[k][7]);
-            }
-          } else {
+        for (int q = 0; q < C_SPX / 4; ++q) {
+          const float4 v = s4[q];
+          sp[4 * q] = v.x; sp[4 * q + 1] = v.y; sp[4 * q + 2] = v.z; sp[4 * q + 3] = v.w;
+        }
+        float cc[NC > 0 ? NC : 1];
 #pragma unroll
-            for (int k = 0; k < K; ++k)
+        for (int k = 0; k < NC; ++k) cc[k] = fmaf(-sp[NP + k], S[0], S[k + 1]);
+        float w0 = sp[NS] * S[0];
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (gx0 + i < W) wrow[k * wo.plane + q + i] = wv[k][i];
+        for (int a = 0; a < NC; ++a) {
+          float tt = 0.0f;
+#pragma unroll
+          for (int bq = 0; bq < NC; ++bq) {
+            const int lo = a < bq ? a : bq, hi = a < bq ? bq : a;
+            tt = fmaf(sp[lo * NC - lo * (lo - 1) / 2 + (hi - lo)], cc[bq], tt);
           }
+          wv[a + 1][i] = tt;
+          w0 = fmaf(-sp[NP + a], tt, w0);
+        }
+        wv[0][i] = w0;
+      }
+      if (lok) {
+        float* wrow = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)y * wo.pitch + x0 + xs;
+        if (full) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            float4* d4 = reinterpret_cast<float4*>(wrow + k * wo.plane);
+            d4[0] = make_float4(wv[k][0], wv[k][1], wv[k][2], wv[k][3]);
+            d4[1] = make_float4(wv[k][4], wv[k][5], wv[k][6], wv[k][7]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int i = 0; i < C_HSEG; ++i)
+              if (x0 + xs + i < W) wrow[k * wo.plane + i] = wv[k][i];
         }
       }
       named_arrive(3 + b, NALL);                   // buffer b free again
@@ -204,19 +297,33 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
   }
 }
 
-template <int NC>
-cudaError_t coef3_impl(const float* G, const float* stats, const float* vol, float* wbuf, WLayout wo, int W, int H,
-                       int r, int L, float lam0, cudaStream_t st) {
+template <int NC, int R>
+cudaError_t coef3_r(const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo, int W, int H,
+                    int r, int L, float lam0, cudaStream_t st) {
   using Gm = CoefGeom<NC>;
-  cudaError_t e = cudaFuncSetAttribute(k_coef3<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(k_coef3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
   if (e != cudaSuccess) return e;
   // band height: enough CTAs to fill 148 SMs at least ~4 times, but long enough to amortise the warm-up
   const int strips = (W + C_TX - 1) / C_TX, batches = (L + C_LB - 1) / C_LB;
   int BH = 128;
   while (BH > 32 && (long long)strips * ((H + BH - 1) / BH) * batches < 4 * 148) BH /= 2;
   dim3 grid(strips, (H + BH - 1) / BH, batches);
-  k_coef3<NC><<<grid, Gm::THREADS, Gm::SMEM, st>>>(G, stats, vol, wbuf, wo, W, H, r, L, BH, lam0);
+  k_coef3<NC, R><<<grid, Gm::THREADS, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),
+                                                      G, stats, wbuf, wo, W,
+                                                      H, r, L, BH, lam0);
   return cudaGetLastError();
+}
+
+template <int NC>
+cudaError_t coef3_impl(const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo, int W,
+                       int H, int r, int L, float lam0, cudaStream_t st) {
+  switch (r) {
+    case 2: return coef3_r<NC, 2>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 4: return coef3_r<NC, 4>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 7: return coef3_r<NC, 7>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 9: return coef3_r<NC, 9>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+    default: return coef3_r<NC, 0>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+  }
 }
 
 }  // namespace v3
