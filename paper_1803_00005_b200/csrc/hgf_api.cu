@@ -38,6 +38,7 @@ struct hgf_ctx {
   CUtensorMap tm_w;            // TMA descriptor over wbuf (padded layout), box agg3_box(r) x (n+1)
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
+  CUtensorMap tm_g;            // TMA descriptor over G (dims W, H, n; box 88 x 1 x n) for k_coef3
   std::string err;
   // tracing (hgf_set_profiling / hgf_profile_read)
   bool profiling = false;
@@ -180,7 +181,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
       CUtensorMap tm_vol;
       if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, 88, 1, 32))
         return cudaErrorInvalidValue;
-      return hgf::launch_coef_v3(h->n, &tm_vol, h->G, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
+      return hgf::launch_coef_v3(h->n, &tm_vol, &h->tm_g, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                  h->stream);
     }
     if (h->fast)
@@ -316,8 +317,9 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->wlay = flat;
   }
   {
-    const char* f = std::getenv("HGF_COEF3");   // opt-in until it beats k_coef2 (profiles/r01_*)
-    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && (f && f[0] == '1');
+    const char* f = std::getenv("HGF_COEF3");   // default on; HGF_COEF3=0 selects k_coef2
+    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
+                encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
   }
   *out = h;
   return HGF_OK;

@@ -33,7 +33,7 @@ constexpr int C_TX = 64;                    // owned columns per strip
 constexpr int C_LB = 32;                    // labels per CTA batch
 constexpr int C_LG = 8;                     // labels per V thread
 constexpr int C_NG = C_LB / C_LG;           // V label groups
-constexpr int C_HSEG = 8;                   // pixels per H thread
+constexpr int C_HSEG = 16;                  // pixels per H thread (two store groups of 8)
 constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
 constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = 16 labels x 2 segments
 constexpr int C_RMAX = 9;
@@ -47,13 +47,14 @@ struct CoefGeom {
   static constexpr int K = NC + 1, NP = NC * (NC + 1) / 2, NS = NP + NC;
   static_assert(NS + 1 <= C_SPX, "statistics + kappa must fit the per-pixel slot");
   static constexpr int CXMAX = C_TX + 2 * C_RMAX;         // V columns (strip + halo), max 82
-  static constexpr int CP = CXMAX | 1;                      // SMEM column pitch (odd)
+  static constexpr int CP = CXMAX;                          // SMEM column pitch
   static constexpr int LSTRIDE = K * CP + ((K * CP) % 2 == 0 ? 1 : 0);  // floats per label (odd)
   static constexpr int VROW = C_LB * LSTRIDE;               // floats per V row buffer
   static constexpr int SROW = C_NSEG * C_SSEG;              // statistics row
-  // one TMA stage: entering + leaving rows of the 32 labels' cost slices (128-byte aligned sizes)
-  static constexpr int PROW = C_LB * C_BXP;
-  static constexpr int STAGE = 2 * PROW;
+  // one TMA stage: entering + leaving rows of the 32 labels' cost slices and of the NC guidance planes
+  // (every TMA destination 128-byte aligned: sizes rounded to 32 floats)
+  static constexpr int PROW = C_LB * C_BXP, GROW = ((NC > 0 ? NC : 1) * C_BXP + 31) / 32 * 32;
+  static constexpr int STAGE = 2 * PROW + 2 * GROW;
   // per (segment, label): the 2R+1 window sums of the segment's first pixel, computed by the V warps
   static constexpr int ISEG = C_LB * K + 16 + ((C_LB * K) % 32 == 16 ? 16 : 0);  // = 16 banks mod 32
   static constexpr int INI = C_NSEG * ISEG;
@@ -75,7 +76,7 @@ __device__ __forceinline__ void c3_tma_3d(void* dst, const CUtensorMap* tm, int 
 // R > 0: compile-time radius; R == 0: runtime radius r_arg (<= C_RMAX).
 template <int NC, int R>
 __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
-    k_coef3(const __grid_constant__ CUtensorMap tm_vol, const float* __restrict__ G,
+    k_coef3(const __grid_constant__ CUtensorMap tm_vol, const __grid_constant__ CUtensorMap tm_g,
             const float* __restrict__ stats, float* __restrict__ wbuf, WLayout wo, int W, int H, int r_arg, int L,
             int BH, float lam0) {
   using Gm = CoefGeom<NC>;
@@ -114,28 +115,16 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       float* s = stage + (t & 1) * Gm::STAGE;
       const int ye = Y0 - r + t;
       const bool leave = t >= 2 * r + 1;
-      const unsigned bytes = (unsigned)(((leave ? 2 : 1) * Gm::PROW) * 4);
+      const unsigned bytes = (unsigned)(((leave ? 2 : 1) * (Gm::PROW + NC * C_BXP)) * 4);
       cuda::ptx::mbarrier_arrive_expect_tx(cuda::ptx::sem_release, cuda::ptx::scope_cta, cuda::ptx::space_shared,
                                            &bar[t & 1], bytes);
       c3_tma_3d(s, &tm_vol, xt, ye, lb0, &bar[t & 1]);
-      if (leave) c3_tma_3d(s + Gm::PROW, &tm_vol, xt, ye - 2 * r - 1, lb0, &bar[t & 1]);
-    };
-    // guidance values of this column for the entering / leaving rows of step t (label-invariant, prefetched
-    // one step ahead in registers)
-    const int gxc = x0 - r + c;
-    const bool gin = active && gxc >= 0 && gxc < W;
-    auto load_g = [&](int t, float (&ge)[NC > 0 ? NC : 1], float (&gl)[NC > 0 ? NC : 1]) {
-      const int ye = Y0 - r + t, yl = ye - 2 * r - 1;
-      const bool ein = gin && t < nsteps && ye >= 0 && ye < H;
-      const bool lin = gin && t < nsteps && t >= 2 * r + 1 && yl >= 0 && yl < H;
-#pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        ge[k] = ein ? __ldg(G + k * HW + (long long)ye * W + gxc) : 0.0f;
-        gl[k] = lin ? __ldg(G + k * HW + (long long)yl * W + gxc) : 0.0f;
+      if (NC > 0) c3_tma_3d(s + 2 * Gm::PROW, &tm_g, xt, ye, 0, &bar[t & 1]);
+      if (leave) {
+        c3_tma_3d(s + Gm::PROW, &tm_vol, xt, ye - 2 * r - 1, lb0, &bar[t & 1]);
+        if (NC > 0) c3_tma_3d(s + 2 * Gm::PROW + Gm::GROW, &tm_g, xt, ye - 2 * r - 1, 0, &bar[t & 1]);
       }
     };
-    float gen[NC > 0 ? NC : 1], gln[NC > 0 ? NC : 1];
-    load_g(0, gen, gln);
     if (tid == 0) {
       issue(0);
       if (nsteps > 1) issue(1);
@@ -166,14 +155,13 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       while (!cuda::ptx::mbarrier_try_wait_parity(&bar[t & 1], (t >> 1) & 1)) {
       }
       const bool leave = t >= 2 * r + 1;
-      float ge[NC > 0 ? NC : 1], gl[NC > 0 ? NC : 1];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        ge[k] = gen[k];
-        gl[k] = gln[k];
-      }
-      load_g(t + 1, gen, gln);
       if (active) {
+        float ge[NC > 0 ? NC : 1], gl[NC > 0 ? NC : 1];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          ge[k] = s[2 * Gm::PROW + k * C_BXP + cs];
+          gl[k] = leave ? s[2 * Gm::PROW + Gm::GROW + k * C_BXP + cs] : 0.0f;
+        }
 #pragma unroll
         for (int j = 0; j < C_LG; ++j) {
           const float pe = s[(g * C_LG + j) * C_BXP + cs];
@@ -234,7 +222,6 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
     const int l = lb0 + lab;
     const bool lok = l < L;
     const int xs = seg * C_HSEG;                      // first owned pixel (strip-relative)
-    const bool full = x0 + xs + C_HSEG <= W;
     for (int y = Y0; y < Y1; ++y) {
       const int b = (y - Y0) & 1;
       named_sync(1 + b, NALL);
@@ -244,9 +231,12 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       float S[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) S[k] = ip[k];
-      float wv[K][C_HSEG];
+#pragma unroll 1
+      for (int q8 = 0; q8 < C_HSEG; q8 += 8) {
+      float wv[K][8];
 #pragma unroll
-      for (int i = 0; i < C_HSEG; ++i) {
+      for (int ii = 0; ii < 8; ++ii) {
+        const int i = q8 + ii;
         if (i > 0) {
 #pragma unroll
           for (int k = 0; k < K; ++k) S[k] += vr[k * CP + i + 2 * r] - vr[k * CP + i - 1];
@@ -270,14 +260,14 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
             const int lo = a < bq ? a : bq, hi = a < bq ? bq : a;
             tt = fmaf(sp[lo * NC - lo * (lo - 1) / 2 + (hi - lo)], cc[bq], tt);
           }
-          wv[a + 1][i] = tt;
+          wv[a + 1][ii] = tt;
           w0 = fmaf(-sp[NP + a], tt, w0);
         }
-        wv[0][i] = w0;
+        wv[0][ii] = w0;
       }
       if (lok) {
-        float* wrow = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)y * wo.pitch + x0 + xs;
-        if (full) {
+        float* wrow = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)y * wo.pitch + x0 + xs + q8;
+        if (x0 + xs + q8 + 8 <= W) {
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             float4* d4 = reinterpret_cast<float4*>(wrow + k * wo.plane);
@@ -288,9 +278,10 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < K; ++k)
 #pragma unroll
-            for (int i = 0; i < C_HSEG; ++i)
-              if (x0 + xs + i < W) wrow[k * wo.plane + i] = wv[k][i];
+            for (int i = 0; i < 8; ++i)
+              if (x0 + xs + q8 + i < W) wrow[k * wo.plane + i] = wv[k][i];
         }
+      }
       }
       named_arrive(3 + b, NALL);                   // buffer b free again
     }
@@ -298,7 +289,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
 }
 
 template <int NC, int R>
-cudaError_t coef3_r(const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo, int W, int H,
+cudaError_t coef3_r(const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo, int W, int H,
                     int r, int L, float lam0, cudaStream_t st) {
   using Gm = CoefGeom<NC>;
   cudaError_t e = cudaFuncSetAttribute(k_coef3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
@@ -309,20 +300,20 @@ cudaError_t coef3_r(const void* tm_vol, const float* G, const float* stats, floa
   while (BH > 32 && (long long)strips * ((H + BH - 1) / BH) * batches < 4 * 148) BH /= 2;
   dim3 grid(strips, (H + BH - 1) / BH, batches);
   k_coef3<NC, R><<<grid, Gm::THREADS, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),
-                                                      G, stats, wbuf, wo, W,
+                                                      *reinterpret_cast<const CUtensorMap*>(tm_g), stats, wbuf, wo, W,
                                                       H, r, L, BH, lam0);
   return cudaGetLastError();
 }
 
 template <int NC>
-cudaError_t coef3_impl(const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo, int W,
+cudaError_t coef3_impl(const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo, int W,
                        int H, int r, int L, float lam0, cudaStream_t st) {
   switch (r) {
-    case 2: return coef3_r<NC, 2>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
-    case 4: return coef3_r<NC, 4>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
-    case 7: return coef3_r<NC, 7>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
-    case 9: return coef3_r<NC, 9>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
-    default: return coef3_r<NC, 0>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 2: return coef3_r<NC, 2>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 4: return coef3_r<NC, 4>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 7: return coef3_r<NC, 7>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st);
+    case 9: return coef3_r<NC, 9>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st);
+    default: return coef3_r<NC, 0>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st);
   }
 }
 

@@ -153,9 +153,9 @@ cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cuda
 
 namespace hgf {
 
-cudaError_t launch_coef_v3(int n, const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo,
+cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
                            int W, int H, int r, int L, float lam0, cudaStream_t st) {
-#define C3(N) return v3::coef3_impl<N>(tm_vol, G, stats, wbuf, wo, W, H, r, L, lam0, st)
+#define C3(N) return v3::coef3_impl<N>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st)
   switch (n) {
     case 1: C3(1); case 2: C3(2); case 3: C3(3); case 4: C3(4); case 5: C3(5); case 6: C3(6);
     default: return cudaErrorInvalidValue;

@@ -23,7 +23,7 @@ template cudaError_t agg2_impl<HGF_N>(const AggArgs&, cudaStream_t);
 #if HGF_N <= 6
 namespace hgf {
 namespace v3 {
-template cudaError_t coef3_impl<HGF_N>(const void*, const float*, const float*, float*, WLayout, int, int, int, int,
+template cudaError_t coef3_impl<HGF_N>(const void*, const void*, const float*, float*, WLayout, int, int, int, int,
                                        float, cudaStream_t);
 }  // namespace v3
 }  // namespace hgf

@@ -69,12 +69,12 @@ void agg3_box(int R, int* bx, int* by);
 cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
 namespace v3 {
 template <int NC>
-cudaError_t coef3_impl(const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo, int W,
+cudaError_t coef3_impl(const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo, int W,
                        int H, int r, int L, float lam0, cudaStream_t st);
 }  // namespace v3
 // Label-batched marching coefficient kernel (hgf_coef_v3.cuh): n <= 6, r <= 9, padded layout.
-// tm_vol: CUtensorMap over the chunk's cost slices (dims W, H, L; box 88 x 1 x 32); G: guidance planes.
-cudaError_t launch_coef_v3(int n, const void* tm_vol, const float* G, const float* stats, float* wbuf, WLayout wo,
+// tm_vol: CUtensorMap over the chunk's cost slices (dims W, H, L; box 88 x 1 x 32); tm_g over G (box 88 x 1 x n).
+cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
                            int W, int H, int r, int L, float lam0, cudaStream_t st);
 }  // namespace hgf
 

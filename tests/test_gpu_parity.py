@@ -168,10 +168,10 @@ def test_invalid_arguments_fail_loudly():
         h.aggregate_wta(torch.zeros(3, 10, 10, device="cuda"), torch.zeros(2, 10, 11, device="cuda"))
 
 
-@pytest.mark.parametrize("kernel_env", ["HGF_COEF3", "HGF_NO_V3", "HGF_FORCE_V1"])
-def test_kernel_variants_parity(monkeypatch, kernel_env):
-    """Every coefficient/aggregation kernel variant against the oracle (k_coef3, v2 flat layout, v1)."""
-    monkeypatch.setenv(kernel_env, "1")
+@pytest.mark.parametrize("kernel_env,val", [("HGF_COEF3", "0"), ("HGF_NO_V3", "1"), ("HGF_FORCE_V1", "1")])
+def test_kernel_variants_parity(monkeypatch, kernel_env, val):
+    """Every coefficient/aggregation kernel variant against the oracle (k_coef2, v2 flat layout, v1)."""
+    monkeypatch.setenv(kernel_env, val)
     c = synth.config("C2")
     scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
     V = synth.stereo_cost_volume_np(scene, 40)[:, :200, :260].copy()
