@@ -44,7 +44,8 @@ struct AggGeom {
   static constexpr int PLANE = BY * BX;                    // floats per plane in SMEM
   static constexpr int LABEL_FLOATS = K * PLANE;                 // bytes landed by one slice's TMA / 4
   static constexpr int BUF_STRIDE = (LABEL_FLOATS + 31) / 32 * 32; // keeps every TMA destination 128-B aligned
-  static constexpr int NBUF = (2 * BUF_STRIDE * 4 <= 200 * 1024) ? 2 : 1;
+  // one slice buffer per CTA and two CTAs per SM: the co-resident CTA hides this one's TMA wait
+  static constexpr int NBUF = 1;
   static constexpr int NV4 = (KX + 2 * R + 3) / 4;        // 128-bit loads per owner row segment
   static_assert(KX * (NSEG - 1) + 4 * NV4 <= BX, "owner loads stay inside the row");
   static_assert(BX <= 256 && BY <= 256, "TMA box limits");
@@ -73,7 +74,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 }
 
 template <int NC, int R>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     k_agg3(const __grid_constant__ CUtensorMap tmw, const float* __restrict__ G, int W, int H, int pad, int L, int label_base,
            float* __restrict__ filtered_out, int do_wta, int first, int last, float* __restrict__ best_cost,
            int32_t* __restrict__ best_label, int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out,
