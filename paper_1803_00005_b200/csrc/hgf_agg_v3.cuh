@@ -16,6 +16,13 @@
 //   * horizontal pass + Z + WTA by owner threads (one row x 8 pixels each) that keep G, 1/N and the
 //     running (min, argmin) in registers; 128-bit shared loads, conflict-free by construction
 //     (8 lanes of a quarter-warp read 8 different rows; the row pitch BX has BX/4 odd).
+//
+// IL = true reads the label-interleaved coefficient layout written by k_coef3 (WLayout::il): a rank-5
+// tensor map (16 px, 32 labels, x groups, y, planes) with box (16, 1, BX/16, BY, K) lands the same
+// [k][y][x] tile (BX a multiple of 32) with the 64-byte TMA swizzle: the 16-byte chunk c of 64-byte row
+// R sits at chunk c ^ ((R >> 1) & 3), i.e. float index f -> f ^ ((f >> 3) & 12).  The swizzle keeps both
+// passes conflict-free without a padded pitch; owners then map a quarter-warp to 4 rows x 2 segments that
+// are 16 pixels apart (tools/swizzle_banks.py checks every access pattern).
 #pragma once
 #include <cuda.h>
 
@@ -35,11 +42,11 @@ __host__ __device__ constexpr int box_pitch(int wx) {
   return b;
 }
 
-template <int NC, int R>
+template <int NC, int R, bool IL = false>
 struct AggGeom {
   static constexpr int K = NC + 1;
   static constexpr int WX = TX + 2 * R;
-  static constexpr int BX = box_pitch(WX);
+  static constexpr int BX = IL ? (WX + 31) / 32 * 32 : box_pitch(WX);   // IL: whole 128-B rows
   static constexpr int BY = TY + 2 * R;
   static constexpr int PLANE = BY * BX;                    // floats per plane in SMEM
   static constexpr int LABEL_FLOATS = K * PLANE;                 // bytes landed by one slice's TMA / 4
@@ -49,7 +56,14 @@ struct AggGeom {
   static constexpr int NV4 = (KX + 2 * R + 3) / 4;        // 128-bit loads per owner row segment
   static_assert(KX * (NSEG - 1) + 4 * NV4 <= BX, "owner loads stay inside the row");
   static_assert(BX <= 256 && BY <= 256, "TMA box limits");
+  static_assert(!IL || (NBUF == 1 && (BX % 16) == 0), "swizzled tile: one 1024-B aligned buffer");
 };
+
+// SMEM float index of logical tile element f under the 64-byte TMA swizzle (identity without it).
+template <bool IL>
+__device__ __forceinline__ int swz(int f) {
+  return IL ? (f ^ ((f >> 3) & 12)) : f;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -73,24 +87,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
   cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, dst, tm, c, bar);
 }
 
-template <int NC, int R>
+template <int NC, int R, bool IL>
 __global__ void __launch_bounds__(THREADS, 2)
     k_agg3(const __grid_constant__ CUtensorMap tmw, const float* __restrict__ G, int W, int H, int pad, int L, int label_base,
            float* __restrict__ filtered_out, int do_wta, int first, int last, float* __restrict__ best_cost,
            int32_t* __restrict__ best_label, int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out,
            int64_t* __restrict__ keys_out) {
-  using Gm = AggGeom<NC, R>;
+  using Gm = AggGeom<NC, R, IL>;
   constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PLANE = Gm::PLANE, NBUF = Gm::NBUF, NV4 = Gm::NV4;
   constexpr unsigned BYTES = Gm::LABEL_FLOATS * 4u;
   // Dynamic SMEM: NBUF slice buffers (each BUF_STRIDE floats, 128-B aligned) followed by the mbarriers.
   // Indexing the __shared__ array directly keeps every access in the shared state space (LDS/STS).
-  extern __shared__ __align__(128) float buf[];
+  extern __shared__ __align__(1024) float buf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(buf + NBUF * Gm::BUF_STRIDE);
   const int tid = threadIdx.x;
   // Tiles start at x0 = 64*bx - XSHIFT so that the TMA x coordinate x0 - R is a multiple of 4 (16 bytes):
   // TMA traps on x offsets that are not 16-byte aligned (tools/tma_test2.cu); negative coordinates and
   // the out-of-bounds zero fill are fine, and implement the clipped windows.
-  constexpr int XSHIFT = (4 - R % 4) % 4;
+  constexpr int XALIGN = IL ? 16 : 4;   // IL: x groups of 16 pixels
+  constexpr int XSHIFT = (XALIGN - R % XALIGN) % XALIGN;
   // Grouped tile order: consecutive CTAs walk down a column of GY tiles before moving right, so the ~148
   // CTAs resident at once cover a compact ~12 x 12-tile block and the R-halos they share (the coefficient
   // tiles overlap by 2R) are L2 hits instead of repeated HBM reads (ncu r01: 1.64x re-read with row order).
@@ -114,16 +129,24 @@ __global__ void __launch_bounds__(THREADS, 2)
     fence_barrier_init();
   }
   __syncthreads();
-  if (tid == 0 && L > 0) {
-    mbar_expect_tx(&bar[0], BYTES);
-    tma_load_3d(buf, &tmw, tx0, ty0, 0, &bar[0]);
-  }
+  // label l of the chunk: plane coordinate l * K (planar) or group coordinates (l % 32, (l / 32) * K) (IL)
+  auto load = [&](float* dst, int l, uint64_t* bb) {
+    mbar_expect_tx(bb, BYTES);
+    if (IL) {
+      const int32_t c[5] = {0, l % kWGroupLabels, tx0 / kWGroupPx, ty0, (l / kWGroupLabels) * K};
+      cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, dst, &tmw, c, bb);
+    } else {
+      tma_load_3d(dst, &tmw, tx0, ty0, l * K, bb);
+    }
+  };
+  if (tid == 0 && L > 0) load(buf, 0, &bar[0]);
 
   // owner role: row oy, pixels x0 + 8*seg + [0, 8)
   const bool is_owner = tid < NOWN;
   const int wq = tid >> 5, ln = tid & 31;
-  const int oy = (ln & 7) + 8 * (wq % 3);
-  const int seg = (ln >> 3) + 4 * (wq / 3);
+  // planar: a quarter-warp = 8 rows of one segment (odd BX/4 pitch); IL: 4 rows x segments s, s + 2
+  const int oy = IL ? (ln & 3) + 4 * wq : (ln & 7) + 8 * (wq % 3);
+  const int seg = IL ? ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1) : (ln >> 3) + 4 * (wq / 3);
   const int gy = y0 + oy;
   float g[NC > 0 ? NC : 1][KX];
   float invN[KX], best[KX];
@@ -152,24 +175,23 @@ __global__ void __launch_bounds__(THREADS, 2)
     mbar_wait(&bar[b], parity);
     if (NBUF == 2 && tid == 0 && l + 1 < L) {           // prefetch the next slice into the other buffer
       fence_proxy_async();
-      mbar_expect_tx(&bar[b ^ 1], BYTES);
-      tma_load_3d(buf + (b ^ 1) * Gm::BUF_STRIDE, &tmw, tx0, ty0, (l + 1) * K, &bar[b ^ 1]);
+      load(buf + (b ^ 1) * Gm::BUF_STRIDE, l + 1, &bar[b ^ 1]);
     }
     // ---- vertical window sums, in place: rows [0, TY) <- sum of rows [y, y + 2R]
     for (int item = tid; item < K * Gm::WX; item += THREADS) {
       const int k = item / Gm::WX, c = item % Gm::WX;
-      float* colp = lb + k * PLANE + c;
+      const int f0 = k * PLANE + c;
       float col[BY];
 #pragma unroll
-      for (int y = 0; y < BY; ++y) col[y] = colp[y * BX];
+      for (int y = 0; y < BY; ++y) col[y] = lb[swz<IL>(f0 + y * BX)];
       float acc = 0.0f;
 #pragma unroll
       for (int y = 0; y <= 2 * R; ++y) acc += col[y];
-      colp[0] = acc;
+      lb[swz<IL>(f0)] = acc;
 #pragma unroll
       for (int y = 1; y < TY; ++y) {
         acc += col[y + 2 * R] - col[y - 1];
-        colp[y * BX] = acc;
+        lb[swz<IL>(f0 + y * BX)] = acc;
       }
     }
     __syncthreads();
@@ -178,11 +200,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       float z[KX];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const float4* rp = reinterpret_cast<const float4*>(lb + k * PLANE + oy * BX + seg * KX);
+        const int f0 = k * PLANE + oy * BX + seg * KX;
         float f[4 * NV4];
 #pragma unroll
         for (int q = 0; q < NV4; ++q) {
-          const float4 v = rp[q];
+          const float4 v = *reinterpret_cast<const float4*>(lb + swz<IL>(f0 + 4 * q));
           f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
         }
         float acc = 0.0f;
@@ -211,8 +233,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncthreads();
     if (NBUF == 1 && tid == 0 && l + 1 < L) {
       fence_proxy_async();
-      mbar_expect_tx(&bar[0], BYTES);
-      tma_load_3d(buf, &tmw, tx0, ty0, (l + 1) * K, &bar[0]);
+      load(buf, l + 1, &bar[0]);
     }
   }
   if (!do_wta || !is_owner) return;
@@ -232,22 +253,28 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
-template <int NC, int R>
+template <int NC, int R, bool IL>
 size_t agg3_smem_bytes() {
-  using Gm = AggGeom<NC, R>;
+  using Gm = AggGeom<NC, R, IL>;
   return (size_t)Gm::NBUF * Gm::BUF_STRIDE * 4 + 128;
+}
+
+template <int NC, int R, bool IL>
+cudaError_t agg3_launch(const void* tmap, const AggArgs& a, cudaStream_t st) {
+  const size_t smem = agg3_smem_bytes<NC, R, IL>();
+  cudaError_t e = cudaFuncSetAttribute(k_agg3<NC, R, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  constexpr int XALIGN = IL ? 16 : 4;
+  dim3 grid((a.W + (XALIGN - R % XALIGN) % XALIGN + TX - 1) / TX, (a.H + TY - 1) / TY);
+  k_agg3<NC, R, IL><<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.pad, a.L,
+                                             a.label_base, a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
+                                             a.best_label, a.labels_out, a.min_cost_out, a.keys_out);
+  return cudaGetLastError();
 }
 
 template <int NC, int R>
 cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st) {
-  const size_t smem = agg3_smem_bytes<NC, R>();
-  cudaError_t e = cudaFuncSetAttribute(k_agg3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid((a.W + (4 - R % 4) % 4 + TX - 1) / TX, (a.H + TY - 1) / TY);
-  k_agg3<NC, R><<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.pad, a.L,
-                                             a.label_base, a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
-                                             a.best_label, a.labels_out, a.min_cost_out, a.keys_out);
-  return cudaGetLastError();
+  return a.il ? agg3_launch<NC, R, true>(tmap, a, st) : agg3_launch<NC, R, false>(tmap, a, st);
 }
 
 }  // namespace v3

@@ -208,7 +208,20 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
     return false;
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   int bx = 0, by = 0;
-  hgf::agg3_box(h->r, &bx, &by);
+  hgf::agg3_box(h->r, h->wlay.il, &bx, &by);
+  if (h->wlay.il) {
+    // rank 5 over the label-interleaved layout: (16 px, 32 labels, x groups, y, label-batch planes); one box
+    // = one label's K planes of a BX x BY tile, 64-byte inner runs with the matching 64-byte swizzle
+    const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
+    const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
+                                (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * (h->n + 1)};
+    const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * h->H};
+    const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, (cuuint32_t)(h->n + 1)};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return encode(&h->tm_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
                               (cuuint64_t)h->lcap * (h->n + 1)};
   const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
@@ -231,7 +244,7 @@ hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int l
     hgf::AggArgs a{};
     a.G = h->G;
     a.wbuf = h->wbuf;
-    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = h->wlay.pad;
+    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = h->wlay.pad; a.il = h->wlay.il;
     a.label_base = label_offset + c0;
     a.filtered_out = filtered_out ? filtered_out + (long long)c0 * HW : nullptr;
     a.do_wta = do_wta;
@@ -289,21 +302,39 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     const char* g = std::getenv("HGF_NO_V3");
     h->v3agg = h->fast && h->n <= 9 && !(g && g[0] == '1');     // confirmed below once the TMA map exists
   }
-  // coefficient buffer layout: rows pitched to a multiple of 4 floats for the TMA path
-  const hgf::WLayout flat{0, (long long)HW, W, 0};
-  hgf::WLayout padded{};
-  padded.pad = 0;
-  padded.pitch = (W + 3) / 4 * 4;       // 16-byte rows: TMA global strides and the 128-bit stores of k_coef3
-  padded.plane = (long long)H * padded.pitch;
-  padded.origin = 0;
-  h->wlay = h->v3agg ? padded : flat;
-  const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
-  size_t cap = coef_budget_bytes() / per_label;
-  h->lcap = (int)(cap < 1 ? 1 : (cap > 4096 ? 4096 : cap));
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
-      (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess ||
-      (e = cudaMalloc(&h->wbuf, per_label * h->lcap)) != cudaSuccess ||
+      (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess) {
+    cudaGetLastError();
+    release(h);
+    delete h;
+    return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
+  }
+  {
+    const char* f = std::getenv("HGF_COEF3");   // default on; HGF_COEF3=0 selects k_coef2
+    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
+                encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
+  }
+  // coefficient buffer layout: label-interleaved for k_coef3 -> k_agg3, else rows pitched to a multiple of
+  // 4 floats for the TMA aggregation, else flat
+  const hgf::WLayout flat{0, (long long)HW, W, 0, 0, 0};
+  hgf::WLayout padded{};
+  padded.pad = 0;
+  padded.pitch = (W + 3) / 4 * 4;       // 16-byte rows: TMA global strides
+  padded.plane = (long long)H * padded.pitch;
+  padded.origin = 0;
+  hgf::WLayout inter{};
+  inter.il = 1;
+  inter.xg = (W + hgf::kWGroupPx - 1) / hgf::kWGroupPx;
+  inter.plane = (long long)H * inter.xg * hgf::kWGroupPx;   // floats per (label, plane) slot
+  inter.pitch = inter.xg * hgf::kWGroupPx;
+  h->wlay = h->v3coef ? inter : (h->v3agg ? padded : flat);
+  const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
+  size_t cap = coef_budget_bytes() / per_label;
+  cap = cap < 1 ? 1 : (cap > 4096 ? 4096 : cap);
+  if (h->wlay.il) cap = cap < (size_t)hgf::kWGroupLabels ? hgf::kWGroupLabels : cap / hgf::kWGroupLabels * hgf::kWGroupLabels;
+  h->lcap = (int)cap;
+  if ((e = cudaMalloc(&h->wbuf, per_label * h->lcap)) != cudaSuccess ||
       (e = cudaMalloc(&h->best_cost, sizeof(float) * HW)) != cudaSuccess ||
       (e = cudaMalloc(&h->best_label, sizeof(int32_t) * HW)) != cudaSuccess ||
       (e = cudaMemset(h->wbuf, 0, per_label * h->lcap)) != cudaSuccess) {
@@ -313,13 +344,10 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
   }
   if (h->v3agg && !((long long)h->lcap * K <= (1LL << 31) && make_wbuf_tensor_map(h))) {
-    h->v3agg = false;   // no TMA descriptor: the v2 aggregation reads the flat layout (fits the allocation)
+    // no TMA descriptor: v2 coefficients + aggregation on the flat layout (fits the allocation)
+    h->v3agg = false;
+    h->v3coef = false;
     h->wlay = flat;
-  }
-  {
-    const char* f = std::getenv("HGF_COEF3");   // default on; HGF_COEF3=0 selects k_coef2
-    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
-                encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
   }
   *out = h;
   return HGF_OK;
@@ -440,6 +468,7 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
     hgf::AggArgs a{};
     a.G = h->G; a.wbuf = h->wbuf; a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.label_base = l0;
     a.pad = h->wlay.pad;
+    a.il = h->wlay.il;
     a.filtered_out = nullptr; a.do_wta = 1; a.first = (c == 0); a.last = (c == nchunks - 1);
     a.best_cost = h->best_cost; a.best_label = h->best_label; a.labels_out = h->st_labels;
     a.min_cost_out = nullptr; a.keys_out = nullptr;

@@ -34,6 +34,7 @@ constexpr int C_LB = 32;                    // labels per CTA batch
 constexpr int C_LG = 8;                     // labels per V thread
 constexpr int C_NG = C_LB / C_LG;           // V label groups
 constexpr int C_HSEG = 16;                  // pixels per H thread (two store groups of 8)
+static_assert(C_HSEG == kWGroupPx && C_LB == kWGroupLabels, "an H segment is one group of the interleaved layout");
 constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
 constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = 16 labels x 2 segments
 constexpr int C_RMAX = 9;
@@ -71,6 +72,13 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 __device__ __forceinline__ void c3_tma_3d(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
   const int32_t c[3] = {x, y, z};
   cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, dst, tm, c, bar);
+}
+
+// 256-bit global store (sm_100: STG.E.ENL2.256), p 32-byte aligned.
+__device__ __forceinline__ void st_global_v8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
 }
 
 // R > 0: compile-time radius; R == 0: runtime radius r_arg (<= C_RMAX).
@@ -265,7 +273,18 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
         }
         wv[0][ii] = w0;
       }
-      if (lok) {
+      if (wo.il) {
+        // label-interleaved layout: this lane's 16-pixel segment is one group; 32-byte stores, and the 16
+        // labels of the half-warp cover one contiguous 1 KB run (see WLayout)
+        const int grp = (x0 + xs) / kWGroupPx;
+        if (lok && grp < wo.xg) {
+          float* wg = wbuf + (((long long)blockIdx.z * K * H + y) * wo.xg + grp) * (kWGroupPx * kWGroupLabels) +
+                      lab * kWGroupPx + q8;
+          const long long kstride = (long long)H * wo.xg * (kWGroupPx * kWGroupLabels);
+#pragma unroll
+          for (int k = 0; k < K; ++k) st_global_v8(wg + k * kstride, wv[k]);
+        }
+      } else if (lok) {
         float* wrow = wbuf + wo.origin + (long long)l * K * wo.plane + (long long)y * wo.pitch + x0 + xs + q8;
         if (x0 + xs + q8 + 8 <= W) {
 #pragma unroll

@@ -31,14 +31,21 @@ __device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
   return static_cast<int64_t>(pack_key(cost, label) ^ 0x8000000000000000ull);
 }
 
-// Layout of the per-slice coefficient buffer: element (label l, plane k, y, x) of a chunk lives at
-// origin + (l*(n+1) + k)*plane + y*pitch + x.  The v3 aggregation pads it with a zero top/left margin
-// (TMA tiles are then fetched at non-negative coordinates).
+// Layout of the per-slice coefficient buffer.
+// Planar (il == 0): element (label l, plane k, y, x) of a chunk lives at
+//   origin + (l*(n+1) + k)*plane + y*pitch + x.
+// Label-interleaved (il == 1, k_coef3 -> k_agg3): 32 labels share each 16-pixel group,
+//   ((((l/32)*(n+1) + k)*H + y)*xg + x/16)*512 + (l%32)*16 + x%16,
+// so the 16 labels of a k_coef3 half-warp store one contiguous 1 KB run per instruction, and k_agg3's TMA
+// still reads 64-byte runs of one label (16 pixels) per request.
+constexpr int kWGroupPx = 16, kWGroupLabels = 32;
 struct WLayout {
   long long origin;   // = pad * pitch + pad
   long long plane;
   int pitch;          // multiple of 4 in the padded layout (16-byte rows)
   int pad;            // zero margin above / left of the image (0 = flat layout; else roundup(r, 4))
+  int il;             // 1 = label-interleaved layout
+  int xg;             // 16-pixel groups per row (il == 1)
 };
 
 // Number of statistics planes stored per pixel for n channels: P' (upper triangle) + nu.

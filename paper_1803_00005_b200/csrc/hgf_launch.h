@@ -12,6 +12,7 @@ struct AggArgs {
   const float* wbuf;
   int W, H, r, L, label_base;
   int pad;   // zero margin of the coefficient layout (v3 aggregation)
+  int il;    // label-interleaved coefficient layout (WLayout::il)
   float* filtered_out;
   int do_wta, first, last;
   float* best_cost;
@@ -65,7 +66,8 @@ template <int NC, int R>
 cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st);
 }  // namespace v3
 // Box of the v3 aggregation TMA for radius R: {BX, BY} (x extent, y extent); z extent = n + 1.
-void agg3_box(int R, int* bx, int* by);
+// il = 1: label-interleaved layout (BX a multiple of 32 pixels; tensor-map box {16, 1, BX/16, BY, n+1}).
+void agg3_box(int R, int il, int* bx, int* by);
 cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
 namespace v3 {
 template <int NC>

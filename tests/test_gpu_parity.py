@@ -118,10 +118,13 @@ def test_deterministic_and_label_offset_and_permutation():
     assert np.array_equal(c["filtered"], a["filtered"][perm])          # per-slice arithmetic independent of l
 
 
-def test_chunked_equals_single_chunk(monkeypatch):
-    I, V = synth.iid_volume(512, 300, 5, 3, seed=6)                    # 4.3 MB of coefficients per label
+@pytest.mark.parametrize("coef3", ["1", "0"])
+def test_chunked_equals_single_chunk(monkeypatch, coef3):
+    """1 MiB budget: 32-label chunks (the interleaved k_coef3 layout's minimum) or 1-label chunks (planar)."""
+    monkeypatch.setenv("HGF_COEF3", coef3)
+    I, V = synth.iid_volume(512, 300, 40, 3, seed=6)                   # 4.3 MB of coefficients per label
     a = _run(I, V, 2, 5, 0.05)
-    monkeypatch.setenv("HGF_COEF_BUDGET_MB", "1")                      # 1 MiB -> 1-label chunks
+    monkeypatch.setenv("HGF_COEF_BUDGET_MB", "1")
     b = _run(I, V, 2, 5, 0.05)
     assert b["launches"] > a["launches"]
     for k in ("filtered", "labels", "min_cost", "keys"):

@@ -1,0 +1,68 @@
+"""Shared-memory bank check for k_agg3's tile under the 64-byte TMA swizzle (IL layout) and the planar
+odd-pitch tile: counts wavefronts per quarter-warp for the owner LDS.128 pattern and ways per warp for the
+vertical pass.  Usage: python tools/swizzle_banks.py [R]
+"""
+import sys
+
+TX, TY, KX = 64, 24, 8
+
+
+def swz(f):
+    return f ^ ((f >> 3) & 12)
+
+
+def owner(ln, wq, il):
+    if il:
+        return (ln & 3) + 4 * wq, ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1)
+    return (ln & 7) + 8 * (wq % 3), (ln >> 3) + 4 * (wq // 3)
+
+
+def lds128_wavefronts(addrs):
+    tot = 0
+    for q in range(4):
+        banks = {}
+        for a in addrs[8 * q:8 * q + 8]:
+            for j in range(4):
+                banks.setdefault((a + j) % 32, set()).add((a + j) // 32)
+        tot += max(len(v) for v in banks.values())
+    return tot
+
+
+def main():
+    R = int(sys.argv[1]) if len(sys.argv) > 1 else 9
+    K = 7
+    WX, BY = TX + 2 * R, TY + 2 * R
+    nv4 = (KX + 2 * R + 3) // 4
+    for il in (False, True):
+        if il:
+            BX = (WX + 31) // 32 * 32
+            f = swz
+        else:
+            BX = (WX + 3) // 4 * 4
+            while (BX // 4) % 2 == 0:
+                BX += 4
+            f = (lambda v: v)
+        worst = 0
+        for wq in range(TY * (TX // KX) // 32):
+            for k in range(K):
+                for q in range(nv4):
+                    addrs = []
+                    for ln in range(32):
+                        oy, seg = owner(ln, wq, il)
+                        addrs.append(f((k * BY + oy) * BX + seg * KX + 4 * q))
+                    worst = max(worst, lds128_wavefronts(addrs))
+        vworst = 0
+        for w0 in range(0, K * WX, 32):
+            for y in range(BY):
+                banks = {}
+                for item in range(w0, min(w0 + 32, K * WX)):
+                    k, c = divmod(item, WX)
+                    a = f((k * BY + y) * BX + c)
+                    banks.setdefault(a % 32, set()).add(a // 32)
+                vworst = max(vworst, max(len(v) for v in banks.values()))
+        print(f"R={R} {'IL/swizzle64' if il else 'planar'}: BX={BX} owner LDS.128 worst {worst} wavefronts "
+              f"(ideal 4); vertical pass worst {vworst}-way")
+
+
+if __name__ == "__main__":
+    main()
