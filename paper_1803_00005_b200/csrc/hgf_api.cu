@@ -1,5 +1,6 @@
 // C ABI of the HGF hot path (declared in include/hgf.h).  Validation, scratch ownership, stream
 // handling and launch sequencing; every step of the path runs in the kernels of hgf_kernels.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -35,7 +36,7 @@ struct hgf_ctx {
   int launches = 0;
   bool fast = false;           // v2 fast-path kernels usable for (m, d, r)
   bool v3agg = false;          // TMA-fed v3 aggregation usable (n <= 9, r <= 9, W % 4 == 0)
-  CUtensorMap tm_w;            // TMA descriptor over wbuf (padded layout), box agg3_box(r) x (n+1)
+  CUtensorMap tm_w[2];         // TMA descriptors over wbuf for k_agg3's two plane groups
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
   CUtensorMap tm_g;            // TMA descriptor over G (dims W, H, n; box 88 x 1 x n) for k_coef3
@@ -139,7 +140,9 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
-    return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->stream);
+    const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+    return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->v3coef ? 1 : 0, lam0,
+                             h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
   return HGF_OK;
@@ -193,7 +196,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
 
 cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
   return traced(h, HGF_KC_AGG, h->stream, [&] {
-    if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, &h->tm_w, a, h->stream);
+    if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, h->tm_w, a, h->stream);
     return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
   });
 }
@@ -209,28 +212,35 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   int bx = 0, by = 0;
   hgf::agg3_box(h->r, h->wlay.il, &bx, &by);
-  if (h->wlay.il) {
-    // rank 5 over the label-interleaved layout: (16 px, 32 labels, x groups, y, label-batch planes); one box
-    // = one label's K planes of a BX x BY tile, 64-byte inner runs with the matching 64-byte swizzle
-    const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
-    const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
-                                (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * (h->n + 1)};
-    const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * h->H};
-    const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, (cuuint32_t)(h->n + 1)};
-    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    return encode(&h->tm_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const int K = h->n + 1, KA = hgf::agg3_ka(K);
+  for (int grp = 0; grp < 2; ++grp) {
+    const cuuint32_t planes = (cuuint32_t)(grp == 0 ? KA : K - KA);
+    CUresult r;
+    if (h->wlay.il) {
+      // rank 5 over the label-interleaved layout: (16 px, 32 labels, x groups, y, label-batch planes); one
+      // box = one label's planes of a BX x BY tile, 64-byte inner runs with the matching 64-byte swizzle
+      const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
+      const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
+                                  (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * K};
+      const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * h->H};
+      const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, planes};
+      const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+      r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
+                                  (cuuint64_t)h->lcap * K};
+      const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
+      const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, planes};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->wbuf, dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) return false;
   }
-  const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
-                              (cuuint64_t)h->lcap * (h->n + 1)};
-  const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)(h->n + 1)};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode(&h->tm_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->wbuf, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return true;
 }
 
 // Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
@@ -304,7 +314,8 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   }
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
-      (e = cudaMalloc(&h->stats, sizeof(float) * hgf::stats_planes(h->n) * HW)) != cudaSuccess) {
+      (e = cudaMalloc(&h->stats, sizeof(float) * std::max(hgf::stats_planes(h->n), hgf::kStatsAos) * HW)) !=
+          cudaSuccess) {
     cudaGetLastError();
     release(h);
     delete h;

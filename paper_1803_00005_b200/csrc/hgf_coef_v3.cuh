@@ -101,7 +101,6 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
   const int x0 = blockIdx.x * C_TX;
   const int Y0 = blockIdx.y * BH, Y1 = min(H, Y0 + BH);
   const int lb0 = blockIdx.z * C_LB;
-  const long long HW = (long long)H * W;
   const int CX = C_TX + 2 * r;                    // V columns used: image x = x0 - r + c
   const int xt = ((x0 - r) >> 2) << 2;            // TMA x start (16-byte aligned; arithmetic shift floors)
   const int sh = (x0 - r) - xt;                   // SMEM column of V column 0
@@ -142,18 +141,21 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
     for (int j = 0; j < C_LG; ++j)
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[j][k] = 0.0f;
-    // statistics of output row y for this thread's share of the strip (prefetched one row ahead)
-    constexpr int SPT = ((NS + 1) * C_TX + NV - 1) / NV;
-    float spre[SPT];
+    // statistics of output row y for the strip, prefetched one row ahead: k_stats2 stores them per pixel
+    // (C_SPX floats: NS statistics, then kappa), so the strip's row is one contiguous run of 16-byte
+    // chunks -> coalesced 128-bit loads and conflict-free 128-bit stores into the segment-padded srow.
+    // Pixels beyond W read as zero, which makes their coefficients zero (the interleaved layout's padding).
+    constexpr int SCH = C_SPX / 4;                       // 16-byte chunks per pixel
+    constexpr int SPT = (C_TX * SCH + NV - 1) / NV;
+    float4 spre[SPT];
     auto load_stats = [&](int y) {
 #pragma unroll
       for (int q = 0; q < SPT; ++q) {
         const int e = tid + q * NV;
-        const int s = e / C_TX, x = e % C_TX, gx = x0 + x;
-        float v = 0.0f;
-        if (e < (NS + 1) * C_TX && y < Y1 && gx < W)
-          v = (s < NS) ? __ldg(stats + s * HW + (long long)y * W + gx)
-                       : 1.0f / (lam0 + (float)window_count(y, gx, H, W, r));
+        const int x = e / SCH;
+        float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (e < C_TX * SCH && y < Y1 && x0 + x < W)
+          v = __ldg(reinterpret_cast<const float4*>(stats + ((long long)y * W + x0) * C_SPX) + e);
         spre[q] = v;
       }
     };
@@ -199,17 +201,19 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < SPT; ++q) {
         const int e = tid + q * NV;
-        if (e < (NS + 1) * C_TX) {
-          const int sidx = e / C_TX, x = e % C_TX;
-          sdst[(x / C_HSEG) * C_SSEG + (x % C_HSEG) * C_SPX + sidx] = spre[q];
+        if (e < C_TX * SCH) {
+          const int x = e / SCH, c4 = e % SCH;
+          *reinterpret_cast<float4*>(sdst + (x / C_HSEG) * C_SSEG + (x % C_HSEG) * C_SPX + 4 * c4) = spre[q];
         }
       }
       // window sums of every (segment, label, plane) at the segment's first pixel: the H warps start their
       // sliding windows from these instead of summing 2R+1 columns each (moves ~1/4 of the H work here)
       named_sync(C_BAR_V, NV);
       for (int item = tid; item < C_NSEG * C_LB * K; item += NV) {
-        const int sg = item / (C_LB * K), rem = item % (C_LB * K);
-        const float* colp = vrow + b * Gm::VROW + (rem / K) * LSTRIDE + (rem % K) * CP + sg * C_HSEG;
+        // lanes walk labels (odd LSTRIDE: conflict-free loads; stride-K stores into ini: conflict-free)
+        const int lab = item % C_LB, sk = item / C_LB, k = sk % K, sg = sk / K;
+        const int rem = lab * K + k;
+        const float* colp = vrow + b * Gm::VROW + lab * LSTRIDE + k * CP + sg * C_HSEG;
         float a = 0.0f;
         if (R > 0) {
 #pragma unroll

@@ -23,8 +23,10 @@ struct AggArgs {
 };
 
 cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st);
-cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode,
-                         cudaStream_t st);
+// aos = 1: per-pixel records of kStatsAos floats (statistics, then kappa = 1/(lam0f + N)) for k_coef3;
+// needs the k_stats2 path (else cudaErrorInvalidValue).
+cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
+                         float lam0f, cudaStream_t st);
 cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H,
                         int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st);
@@ -66,6 +68,8 @@ template <int NC, int R>
 cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st);
 }  // namespace v3
 // Box of the v3 aggregation TMA for radius R: {BX, BY} (x extent, y extent); z extent = n + 1.
+// k_agg3 fetches each slice's K planes as two TMA groups: [0, agg3_ka(K)) and [agg3_ka(K), K).
+__host__ __device__ constexpr int agg3_ka(int K) { return (K + 1) / 2; }
 // il = 1: label-interleaved layout (BX a multiple of 32 pixels; tensor-map box {16, 1, BX/16, BY, n+1}).
 void agg3_box(int R, int il, int* bx, int* by);
 cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
@@ -83,6 +87,7 @@ cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const fl
 namespace hgf {
 namespace st2 {
 template <int NC>
-cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st);
+cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
+                        cudaStream_t st);
 }  // namespace st2
 }  // namespace hgf

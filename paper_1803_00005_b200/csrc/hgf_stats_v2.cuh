@@ -8,6 +8,9 @@
 // are box-filtered 8 pairs at a time: horizontal sliding sums (one thread per (pair, row), float64)
 // then vertical sliding sums (one thread per (pair, column)), so each product costs O(1) adds per
 // output instead of the 2r+1 taps of k_stats.  fp32 x fp32 products are exact in float64.
+//
+// aos = 1 (for k_coef3): per-pixel records of kStatsAos floats instead of planes: the NS statistics, then
+// kappa = 1 / (lambda_0 + N) in float32 (the factor of w_0 in the reassociated Eq13, F10).
 #pragma once
 #include "hgf_common.cuh"
 #include "hgf_launch.h"
@@ -26,7 +29,7 @@ __host__ __device__ inline size_t smem_bytes(int NC, int r) {
 
 template <int NC>
 __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G, float* __restrict__ stats, int W,
-                                                    int H, int r, double lam, int mode) {
+                                                    int H, int r, double lam, int mode, int aos, float lam0f) {
   constexpr int K = NC + 1;
   constexpr int NPAIR = K * (K + 1) / 2 - 1;     // (0,0) is N_p, analytic
   constexpr int NB = (NPAIR + PB - 1) / PB;
@@ -118,7 +121,9 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
   for (int a = 0; a < K; ++a)
 #pragma unroll
     for (int b = 0; b < K; ++b) al[a][b] = 0.0;
-  al[c0][c0] = -inv_lam / (lam + Gm[c0][c0]);                              // F1
+  // F1 (compile-time indices keep Gm / al in registers)
+  if (c0 == 0) al[0][0] = -inv_lam / (lam + Gm[0][0]);
+  else if (K > 1) al[1][1] = -inv_lam / (lam + Gm[1][1]);
 #pragma unroll
   for (int k = 1; k < K; ++k) {
     if (k <= c0) continue;
@@ -146,23 +151,42 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
     al[k][k] = inv_lam * inv_lam * gam;
   }
   const long long p = (long long)gy * W + gx;
+  const double den = (mode == 0) ? (lam + N) : N;
+  if (aos) {
+    float rec[kStatsAos];
+    int s = 0;
+#pragma unroll
+    for (int a = 1; a < K; ++a)
+#pragma unroll
+      for (int b = a; b < K; ++b) rec[s++] = (float)(-lam * al[a][b]);
+#pragma unroll
+    for (int a = 1; a < K; ++a) rec[s++] = (float)(Gm[0][a] / den);
+    rec[s++] = 1.0f / (lam0f + (float)N);
+#pragma unroll
+    for (; s < kStatsAos; ++s) rec[s] = 0.0f;
+    float4* o = reinterpret_cast<float4*>(stats + p * kStatsAos);
+#pragma unroll
+    for (int q = 0; q < kStatsAos / 4; ++q) o[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+    return;
+  }
   int s = 0;
 #pragma unroll
   for (int a = 1; a < K; ++a)
 #pragma unroll
     for (int b = a; b < K; ++b) stats[(long long)(s++) * HW + p] = (float)(-lam * al[a][b]);
-  const double den = (mode == 0) ? (lam + N) : N;
 #pragma unroll
   for (int a = 1; a < K; ++a) stats[(long long)(s++) * HW + p] = (float)(Gm[0][a] / den);
 }
 
 template <int NC>
-cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, cudaStream_t st) {
+cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
+                        cudaStream_t st) {
+  if (aos && stats_planes(NC) + 1 > kStatsAos) return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(NC, r);
   cudaError_t e = cudaFuncSetAttribute(k_stats2<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((W + T - 1) / T, (H + T - 1) / T);
-  k_stats2<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode);
+  k_stats2<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,11 @@ keys = {
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
     "launch__registers_per_thread": "regs",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "lsu_pipe_pct",
+    "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_lgds.avg": "lgds_wavefronts/SM",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_conflicts",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum": "smem_st_conflicts",
+    "lts__t_bytes.sum": "l2_bytes",
 }
 for vals in rows[2:]:
     name = vals[hdr.index("Kernel Name")][:60]
