@@ -22,9 +22,13 @@ constexpr int T = 16;        // output tile side
 constexpr int PB = 8;        // product planes per batch
 constexpr int THREADS = T * T;
 
+constexpr int HP = T + 1;     // row pitch (doubles) of the horizontal sums: lanes walk rows conflict-free
+// Channel tiles: TS rows of pitch TSP = TS rounded up to odd (lanes walk rows in the horizontal pass).
+__host__ __device__ inline int tile_pitch(int r) { return (T + 2 * r) | 1; }
 __host__ __device__ inline size_t smem_bytes(int NC, int r) {
   const int TS = T + 2 * r;
-  return (size_t)(NC + 1) * TS * TS * 4 + (size_t)PB * TS * T * 8 + (size_t)PB * T * T * 8 + 16;
+  return ((size_t)(NC + 1) * TS * tile_pitch(r) * 4 + 15) / 16 * 16 + (size_t)PB * TS * HP * 8 +
+         (size_t)PB * T * T * 8 + 16;
 }
 
 template <int NC>
@@ -34,10 +38,10 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
   constexpr int NPAIR = K * (K + 1) / 2 - 1;     // (0,0) is N_p, analytic
   constexpr int NB = (NPAIR + PB - 1) / PB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int TS = T + 2 * r;
-  float* tiles = reinterpret_cast<float*>(smem_raw);                              // [K][TS][TS]
-  double* hb = reinterpret_cast<double*>(smem_raw + (((size_t)K * TS * TS * 4 + 15) & ~(size_t)15));  // [PB][TS][T]
-  double* vb = hb + PB * TS * T;                                                  // [PB][T][T]
+  const int TS = T + 2 * r, TSP = tile_pitch(r);
+  float* tiles = reinterpret_cast<float*>(smem_raw);                              // [K][TS][TSP]
+  double* hb = reinterpret_cast<double*>(smem_raw + (((size_t)K * TS * TSP * 4 + 15) & ~(size_t)15));  // [PB][TS][HP]
+  double* vb = hb + PB * TS * HP;                                                 // [PB][T][T]
   const int tid = threadIdx.x;
   const int tx = tid % T, ty = tid / T;
   const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
@@ -47,7 +51,8 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
     const int c = e / (TS * TS), rem = e % (TS * TS);
     const int yy = y0 - r + rem / TS, xx = x0 - r + rem % TS;
     const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
-    tiles[e] = in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)yy * W + xx)) : 0.0f;
+    tiles[(c * TS + rem / TS) * TSP + rem % TS] =
+        in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)yy * W + xx)) : 0.0f;
   }
 
   double g[NPAIR];
@@ -63,11 +68,11 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
       int i = 0, q = p + 1;
       while (q >= K - i) { q -= K - i; ++i; }
       const int j = i + q;
-      const float* ti = tiles + (i * TS + row) * TS;
-      const float* tj = tiles + (j * TS + row) * TS;
+      const float* ti = tiles + (i * TS + row) * TSP;
+      const float* tj = tiles + (j * TS + row) * TSP;
       double acc = 0.0;
       for (int dx = 0; dx <= 2 * r; ++dx) acc += (double)ti[dx] * (double)tj[dx];
-      double* ho = hb + (pb * TS + row) * T;
+      double* ho = hb + (pb * TS + row) * HP;
       ho[0] = acc;
 #pragma unroll
       for (int c = 1; c < T; ++c) {
@@ -79,14 +84,14 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
     for (int item = tid; item < PB * T; item += THREADS) {
       const int pb = item / T, col = item % T;
       if (bt * PB + pb >= NPAIR) continue;
-      const double* hc = hb + pb * TS * T + col;
+      const double* hc = hb + pb * TS * HP + col;
       double acc = 0.0;
-      for (int dy = 0; dy <= 2 * r; ++dy) acc += hc[dy * T];
+      for (int dy = 0; dy <= 2 * r; ++dy) acc += hc[dy * HP];
       double* vo = vb + pb * T * T + col;
       vo[0] = acc;
 #pragma unroll
       for (int y = 1; y < T; ++y) {
-        acc += hc[(y + 2 * r) * T] - hc[(y - 1) * T];
+        acc += hc[(y + 2 * r) * HP] - hc[(y - 1) * HP];
         vo[y * T] = acc;
       }
     }
