@@ -172,6 +172,11 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   }
 
+  // owner row-segment offsets of plane 0 (swizzled); PLANE/32 is even, so other planes differ by bit 3 at most
+  static_assert(!IL || ((PLANE / 32) & 1) == 0, "plane swizzle phase");
+  int ofs[NV4];
+#pragma unroll
+  for (int q = 0; q < NV4; ++q) ofs[q] = swz<IL>(oy * BX + seg * KX + 4 * q);
   float z[KX];
 #pragma unroll 1
   for (int l = 0; l < L; ++l) {
@@ -185,17 +190,22 @@ __global__ void __launch_bounds__(THREADS, 2)
         const int kk = item / Gm::VX, c = item % Gm::VX;
         if (c >= Gm::WX) continue;
         const int f0 = kk * PLANE + c;
+        // swizzled address of row y: (f0 ^ m(y)) + y*BX, the XOR mask m depending only on y mod 4
+        // (BX is a multiple of 32 floats, so adding y*BX never carries into the swizzled bits)
+        int fb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fb[j] = IL ? (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 3) << 2)) : f0;
         float col[BY];
 #pragma unroll
-        for (int y = 0; y < BY; ++y) col[y] = lb[swz<IL>(f0 + y * BX)];
+        for (int y = 0; y < BY; ++y) col[y] = lb[fb[y & 3] + y * BX];
         float acc = 0.0f;
 #pragma unroll
         for (int y = 0; y <= 2 * R; ++y) acc += col[y];
-        lb[swz<IL>(f0)] = acc;
+        lb[fb[0]] = acc;
 #pragma unroll
         for (int y = 1; y < TY; ++y) {
           acc += col[y + 2 * R] - col[y - 1];
-          lb[swz<IL>(f0 + y * BX)] = acc;
+          lb[fb[y & 3] + y * BX] = acc;
         }
       }
       __syncthreads();
@@ -203,11 +213,13 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (is_owner) {
 #pragma unroll
         for (int k = (h == 0 ? 0 : KA); k < (h == 0 ? KA : K); ++k) {
-          const int f0 = (k - k0) * PLANE + oy * BX + seg * KX;
+          // plane kk of the group: swizzle mask of plane 0 flipped in bit 3 when kk * PLANE/32 = 2 mod 4
+          const int kk = k - k0;
+          const int flip = (IL && ((kk * ((PLANE / 32) & 3)) & 3) == 2) ? 8 : 0;
           float f[4 * NV4];
 #pragma unroll
           for (int q = 0; q < NV4; ++q) {
-            const float4 v = *reinterpret_cast<const float4*>(lb + swz<IL>(f0 + 4 * q));
+            const float4 v = *reinterpret_cast<const float4*>(lb + kk * PLANE + (ofs[q] ^ flip));
             f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
           }
           float acc = 0.0f;
