@@ -9,13 +9,15 @@
 //   * TMA (one elected V thread): per step, the entering row (y+R) and the leaving row (y-R-1) of the
 //     32 labels' cost slices and of the n guidance planes land in SMEM (2-stage ring, mbarrier-tracked,
 //     issued two steps ahead).  Rows/labels/columns outside the image read as zero (clipped windows).
-//   * V warps (producers): thread = (column c of the strip plus an R halo, group of 8 labels); it keeps the
-//     vertical running sums V_k(c) = sum_{|dy|<=R} G_k p of its 8 labels in registers, and per output row
-//     writes the V row of the 32 labels, plus the row's statistics (27 floats + 1/(lambda_0+N) per pixel,
-//     array-of-structs) to SMEM.
-//   * H warps (consumers): thread = (label, 8-pixel segment); slides the horizontal 2R+1 window over the V
-//     row, reads each pixel's statistics with 128-bit loads shared by 16 lanes (a broadcast), does the
-//     n x n matvec and stores w as 16-byte runs.
+//   * V warps (producers): thread = (column c of the strip plus an R halo, group of 8 labels; groups are
+//     warp-aligned); it keeps the vertical running sums V_k(c) = sum_{|dy|<=R} G_k p of its 8 labels in
+//     registers, and per output row writes the V row of the 32 labels, copies the row's per-pixel
+//     statistics records (k_stats2 aos: 27 floats + kappa = 1/(lambda_0+N)) into SMEM with coalesced
+//     128-bit loads, and sums each segment's first 2R+1-column window (the H warps' starting sums).
+//   * H warps (consumers): lane = label, warp = 16-pixel segment; slides the horizontal 2R+1 window over
+//     the V row, reads each pixel's statistics with 128-bit broadcast loads (one wavefront per warp), does
+//     the n x n matvec and stores w with 32-byte stores into the label-interleaved layout (WLayout::il:
+//     the 32 lanes of one store instruction cover 2 KB contiguous) or 16-byte runs (planar layout).
 //   * V and H warps run one row apart through a double-buffered SMEM V row (named barriers FULL/FREE).
 // Label-invariant data (G, statistics) never costs per-label shared-memory traffic.
 #pragma once
@@ -39,7 +41,7 @@ constexpr int C_NG = C_LB / C_LG;           // V label groups
 constexpr int C_HSEG = 16;                  // pixels per H thread (two store groups of 8)
 static_assert(C_HSEG == kWGroupPx && C_LB == kWGroupLabels, "an H segment is one group of the interleaved layout");
 constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
-constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = 16 labels x 2 segments
+constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = the 32 labels of one segment
 constexpr int C_RMAX = 9;
 constexpr int C_BXP = 88;                   // TMA box width: >= TX + 2*RMAX + 3 (x start rounded down to 16 B)
 constexpr int C_SPX = 28;                   // floats per pixel in the SMEM statistics row (27 + kappa)
@@ -62,7 +64,8 @@ struct CoefGeom {
   // per (segment, label): the 2R+1 window sums of the segment's first pixel, computed by the V warps
   static constexpr int ISEG = C_LB * K + 16 + ((C_LB * K) % 32 == 16 ? 16 : 0);  // = 16 banks mod 32
   static constexpr int INI = C_NSEG * ISEG;
-  static constexpr int NVW = (CXMAX * C_NG + 31) / 32;      // V warps
+  static constexpr int CXP = (CXMAX + 31) / 32 * 32;        // V threads per label group (warp-aligned groups)
+  static constexpr int NVW = (CXP * C_NG + 31) / 32;        // V warps
   static constexpr int THREADS = (NVW + C_NHW) * 32;
   static constexpr size_t SMEM =
       sizeof(float) * (2 * (size_t)STAGE + 2 * (size_t)VROW + 2 * (size_t)SROW + 2 * (size_t)INI) + 64;
@@ -111,8 +114,8 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
 
   if (tid < NV) {
     // ============================ V warps (producers) ============================
-    const int g = tid / CX, c = tid % CX;
-    const bool active = g < C_NG;
+    const int g = tid / Gm::CXP, c = tid % Gm::CXP;  // groups warp-aligned: no bank straddles
+    const bool active = g < C_NG && c < CX;
     const int cs = c + sh;
     if (tid == 0) {
       cuda::ptx::mbarrier_init(&bar[0], 1);
@@ -232,8 +235,10 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
   } else {
     // ============================ H warps (consumers) ============================
     const int h = tid - NV, hw = h >> 5, ln = h & 31;
-    const int lab = (hw & 1) * 16 + (ln & 15);        // label within the batch
-    const int seg = 2 * (hw >> 1) + (ln >> 4);        // 8-pixel segment 0..7
+    // lane = label, warp = segment: each pixel's statistics are one broadcast per warp, and the odd
+    // LSTRIDE keeps the 32 labels' V-row loads conflict-free
+    const int lab = ln;                               // label within the batch
+    const int seg = hw;                               // 16-pixel segment 0..3
     const int l = lb0 + lab;
     const bool lok = l < L;
     const int xs = seg * C_HSEG;                      // first owned pixel (strip-relative)

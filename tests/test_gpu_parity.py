@@ -49,6 +49,10 @@ CASES = [
     ("one-row", 67, 1, 3, 2, 3, 3, 0.05, "hgf"),
     ("one-pixel", 1, 1, 3, 2, 4, 2, 0.05, "hgf"),
     ("L1", 33, 35, 3, 2, 1, 9, 0.05, "hgf"),
+    # label-interleaved k_coef3 -> k_agg3 path: two strips + a partial 16-pixel group, a partial 32-label batch
+    ("il-n6-L35", 100, 37, 3, 2, 35, 9, 0.05, "hgf"),
+    ("il-n6-r4-gf", 132, 29, 3, 2, 33, 4, 0.05, "gf"),
+    ("il-n3-r7", 68, 40, 3, 1, 40, 7, 1e-3, "hgf"),
 ]
 
 
