@@ -32,7 +32,7 @@ namespace hgf {
 namespace v3 {
 
 #ifndef HGF_EXP
-#define HGF_EXP 0   // timing experiments only: 1 = V warps alone, 2 = H warps alone (wrong results)
+#define HGF_EXP 0   // timing experiments only: 1 = V warps alone, 2 = H warps alone, 3 = neither (wrong results)
 #endif
 constexpr int C_TX = 64;                    // owned columns per strip
 constexpr int C_LB = 32;                    // labels per CTA batch
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       while (!cuda::ptx::mbarrier_try_wait_parity(&bar[t & 1], (t >> 1) & 1)) {
       }
       const bool leave = t >= 2 * r + 1;
-      if (active && HGF_EXP != 2) {
+      if (active && (HGF_EXP & 2) == 0) {
         float ge[NC > 0 ? NC : 1], gl[NC > 0 ? NC : 1];
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       if (y < Y0) continue;
       const int b = (y - Y0) & 1;
       if (y - Y0 >= 2) named_sync(3 + b, NALL);        // H warps released buffer b
-      if (active && HGF_EXP != 2) {
+      if (active && (HGF_EXP & 2) == 0) {
         float* dst = vrow + b * Gm::VROW + (g * C_LG) * LSTRIDE + c;
 #pragma unroll
         for (int j = 0; j < C_LG; ++j)
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
       // window sums of every (segment, label, plane) at the segment's first pixel: the H warps start their
       // sliding windows from these instead of summing 2R+1 columns each (moves ~1/4 of the H work here)
       named_sync(C_BAR_V, NV);
-      for (int item = tid; item < (HGF_EXP == 2 ? 0 : C_NSEG * C_LB * K); item += NV) {
+      for (int item = tid; item < ((HGF_EXP & 2) ? 0 : C_NSEG * C_LB * K); item += NV) {
         // lanes walk labels (odd LSTRIDE: conflict-free loads; stride-K stores into ini: conflict-free)
         const int lab = item % C_LB, sk = item / C_LB, k = sk % K, sg = sk / K;
         const int rem = lab * K + k;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
     for (int y = Y0; y < Y1; ++y) {
       const int b = (y - Y0) & 1;
       named_sync(1 + b, NALL);
-      if (HGF_EXP == 1) {
+      if (HGF_EXP & 1) {
         named_arrive(3 + b, NALL);
         continue;
       }

@@ -34,6 +34,10 @@ def main():
         a[1] += t * UNITS.get(tu, 1e-6)
         a[2] += rd * BYTES.get(ru, 1.0)
         a[3] += wr * BYTES.get(wu, 1.0)
+    # only this library's kernels: the launch list also holds torch's synthetic-input kernels, which run
+    # before the timed region
+    other = {k: v for k, v in agg.items() if not any(pre in k for pre in CLASS)}
+    agg = {k: v for k, v in agg.items() if any(pre in k for pre in CLASS)}
     total = sum(v[1] for v in agg.values())
     lines = [f"# ncu launch list — bench.py ({cfg}), round {rnd}", "",
              "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`"
@@ -48,6 +52,9 @@ def main():
         for pre, cls in CLASS.items():
             if pre in name:
                 traffic[cls] = (rd + wr) / n
+    lines.append("")
+    lines.append(f"Not shown: {sum(v[0] for v in other.values())} torch launches ({sum(v[1] for v in other.values()):.1f} ms)"
+                 " that build the synthetic cost volume before the timed region.")
     os.makedirs("profiles", exist_ok=True)
     open(f"profiles/{rnd}_launches_summary.md", "w").write("\n".join(lines) + "\n")
     tpath = "profiles/ncu_traffic.json"
