@@ -39,6 +39,8 @@ struct hgf_ctx {
   CUtensorMap tm_w[2];         // TMA descriptors over wbuf for k_agg3's two plane groups
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
+  bool v4coef = false;         // tensor-core coefficient kernel (planar layout for k_agg3, n <= 6, r <= 9)
+  CUtensorMap tm_g4;           // TMA descriptor over G for k_coef4 (box kCoef4BoxX x 1 x n)
   CUtensorMap tm_g;            // TMA descriptor over G (dims W, H, n; box 88 x 1 x n) for k_coef3
   std::string err;
   // tracing (hgf_set_profiling / hgf_profile_read)
@@ -141,7 +143,8 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
   if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
     const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
-    return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode, h->v3coef ? 1 : 0, lam0,
+    return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode,
+                             (h->v3coef || h->v4coef) ? 1 : 0, lam0,
                              h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
@@ -179,6 +182,14 @@ bool encode_map_3d(CUtensorMap* tm, const void* base, long long dx, long long dy
 cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
+    if (h->v4coef) {
+      CUtensorMap tm_vol;
+      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H,
+                         hgf::kCoef4BoxX, 1, hgf::kCoef4LB))
+        return cudaErrorInvalidValue;
+      return hgf::launch_coef_v4(h->n, &tm_vol, &h->tm_g4, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc,
+                                 h->stream);
+    }
     if (h->v3coef) {
       // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 88 x 1 x 32 (k_coef3)
       CUtensorMap tm_vol;
@@ -322,8 +333,12 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
   }
   {
-    const char* f = std::getenv("HGF_COEF3");   // default on; HGF_COEF3=0 selects k_coef2
-    h->v3coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
+    // default: k_coef4 (tensor cores); HGF_COEF4=0 selects k_coef3, HGF_COEF3=0 (with HGF_COEF4=0) k_coef2
+    const char* f4 = std::getenv("HGF_COEF4");
+    h->v4coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && h->r <= 9 && !(f4 && f4[0] == '0') &&
+                encode_map_3d(&h->tm_g4, h->G, W, H, h->n, W, (long long)W * H, hgf::kCoef4BoxX, 1, h->n);
+    const char* f = std::getenv("HGF_COEF3");
+    h->v3coef = !h->v4coef && h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
                 encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
   }
   // coefficient buffer layout: label-interleaved for k_coef3 -> k_agg3, else rows pitched to a multiple of
@@ -339,7 +354,10 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   inter.xg = (W + hgf::kWGroupPx - 1) / hgf::kWGroupPx;
   inter.plane = (long long)H * inter.xg * hgf::kWGroupPx;   // floats per (label, plane) slot
   inter.pitch = inter.xg * hgf::kWGroupPx;
-  h->wlay = h->v3coef ? inter : (h->v3agg ? padded : flat);
+  hgf::WLayout lines = padded;          // k_coef4: rows start on 128-byte lines (one line per warp store)
+  lines.pitch = (W + 31) / 32 * 32;
+  lines.plane = (long long)H * lines.pitch;
+  h->wlay = h->v3coef ? inter : (h->v4coef ? lines : (h->v3agg ? padded : flat));
   const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
   size_t cap = coef_budget_bytes() / per_label;
   cap = cap < 1 ? 1 : (cap > 4096 ? 4096 : cap);
@@ -358,6 +376,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     // no TMA descriptor: v2 coefficients + aggregation on the flat layout (fits the allocation)
     h->v3agg = false;
     h->v3coef = false;
+    h->v4coef = false;
     h->wlay = flat;
   }
   *out = h;

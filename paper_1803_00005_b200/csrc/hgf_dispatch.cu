@@ -167,4 +167,14 @@ cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const fl
 #undef C3
 }
 
+cudaError_t launch_coef_v4(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
+                           int W, int H, int r, int L, cudaStream_t st) {
+#define C4(N) return v4::coef4_impl<N>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, st)
+  switch (n) {
+    case 1: C4(1); case 2: C4(2); case 3: C4(3); case 4: C4(4); case 5: C4(5); case 6: C4(6);
+    default: return cudaErrorInvalidValue;
+  }
+#undef C4
+}
+
 }  // namespace hgf

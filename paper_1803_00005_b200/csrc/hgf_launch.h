@@ -82,6 +82,16 @@ cudaError_t coef3_impl(const void* tm_vol, const void* tm_g, const float* stats,
 // tm_vol: CUtensorMap over the chunk's cost slices (dims W, H, L; box 88 x 1 x 32); tm_g over G (box 88 x 1 x n).
 cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
                            int W, int H, int r, int L, float lam0, cudaStream_t st);
+// Tensor-core coefficient kernel (hgf_coef_v4.cuh): n <= 6, r <= 9, planar layout (pitch a multiple of 32),
+// per-pixel statistics records.  tm_vol: box kCoef4BoxX x 1 x kCoef4LB; tm_g: box kCoef4BoxX x 1 x n.
+constexpr int kCoef4BoxX = 152, kCoef4LB = 16;
+namespace v4 {
+template <int NC>
+cudaError_t coef4_impl(const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo, int W,
+                       int H, int r, int L, cudaStream_t st);
+}  // namespace v4
+cudaError_t launch_coef_v4(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
+                           int W, int H, int r, int L, cudaStream_t st);
 }  // namespace hgf
 
 namespace hgf {

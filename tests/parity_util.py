@@ -6,6 +6,8 @@ Filtered costs:  e(p,l) = |Z_gpu - Z_ora| / max(|Z_ora|, 1e-3 s_V) <= 1e-4, s_V 
 Labels:          bit-exact wherever the oracle's top-two gap (Z_(2)-Z_(1)) / max(|Z_(1)|, 1e-3 s_V)
                  exceeds 1e-4, and agreement >= 99.99 % overall.
 """
+import os
+
 import numpy as np
 
 Z_TOL = 1e-4
@@ -24,6 +26,8 @@ def check_z(z_gpu, z_ora, s_v, tol=Z_TOL):
     e = z_error(z_gpu, z_ora, s_v)
     assert np.all(np.isfinite(np.asarray(z_gpu))), "non-finite GPU output"
     worst = float(e.max()) if e.size else 0.0
+    if os.environ.get("HGF_PARITY_REPORT"):
+        print(f"[parity] max normalised error {worst:.3e} (tol {tol:.0e})")
     assert worst <= tol, f"max relative error {worst:.3e} > {tol:.1e}"
     return worst
 
