@@ -73,7 +73,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                                        bytes);
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  while (!cuda::ptx::mbarrier_try_wait_parity(bar, parity)) {
+  // the suspend-time hint parks the waiting warp in hardware instead of spinning through issue slots
+  while (!cuda::ptx::mbarrier_try_wait_parity(bar, parity, uint32_t(kMbarSuspendNs))) {
   }
 }
 __device__ __forceinline__ void fence_barrier_init() {

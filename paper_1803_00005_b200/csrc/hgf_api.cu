@@ -333,9 +333,9 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
   }
   {
-    // default: k_coef4 (tensor cores); HGF_COEF4=0 selects k_coef3, HGF_COEF3=0 (with HGF_COEF4=0) k_coef2
+    // default: k_coef3; HGF_COEF4=1 selects k_coef4 (tensor cores), HGF_COEF3=0 k_coef2
     const char* f4 = std::getenv("HGF_COEF4");
-    h->v4coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && h->r <= 9 && !(f4 && f4[0] == '0') &&
+    h->v4coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && h->r <= 9 && (f4 && f4[0] == '1') &&
                 encode_map_3d(&h->tm_g4, h->G, W, H, h->n, W, (long long)W * H, hgf::kCoef4BoxX, 1, h->n);
     const char* f = std::getenv("HGF_COEF3");
     h->v3coef = !h->v4coef && h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&

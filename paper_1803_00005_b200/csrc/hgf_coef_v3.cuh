@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
     load_stats(Y0);
     for (int t = 0; t < nsteps; ++t) {
       const float* s = stage + (t & 1) * Gm::STAGE;
-      while (!cuda::ptx::mbarrier_try_wait_parity(&bar[t & 1], (t >> 1) & 1)) {
+      while (!cuda::ptx::mbarrier_try_wait_parity(&bar[t & 1], (t >> 1) & 1, uint32_t(kMbarSuspendNs))) {
       }
       const bool leave = t >= 2 * r + 1;
       if (active && (HGF_EXP & 2) == 0) {

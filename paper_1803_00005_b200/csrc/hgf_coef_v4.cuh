@@ -22,6 +22,14 @@
 //     stores w in the planar layout (the 32 lanes of a warp write one 128-byte line per plane).
 // No shared-memory traffic for the horizontal pass, the statistics or the segment start sums: the V-row
 // write (2 words per plane per column) is the only per-label exchange between threads.
+//
+// Status (opt-in, HGF_COEF4=1): parity-green and more accurate than k_coef3 (max normalised error 1.4e-5
+// vs 2.3e-5 on the GPU parity cases), but slower at C4 (29 vs 23 ms per frame).  Measured with HGF_EXP4
+// builds: V warps alone 11.7 ms, + MMAs 21.5 ms, + epilogue 24.4 ms -- the tf32 MMAs (2 x 19 per row, the
+// banded A wastes 7/8 of the K extent) keep the tensor pipe busy ~9 ms per frame and the single B buffer
+// (137 KB for hi + lo) serialises V-row writes with them.  A bf16 hi/lo split halves both (one B buffer of
+// bf16x2 pairs, double-buffered) but its 2^-18 representation error fails the 1e-4 parity bound (1.1e-4
+// on C1); see DESIGN.md §6.
 #pragma once
 #include <cuda.h>
 
@@ -77,7 +85,7 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* tm, int x, in
   cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, dst, tm, c, bar);
 }
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
-  while (!cuda::ptx::mbarrier_try_wait_parity(bar, parity)) {
+  while (!cuda::ptx::mbarrier_try_wait_parity(bar, parity, uint32_t(kMbarSuspendNs))) {   // parked, not spinning
   }
 }
 

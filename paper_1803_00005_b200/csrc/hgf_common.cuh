@@ -39,6 +39,9 @@ __device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
 // so the 16 labels of a k_coef3 half-warp store one contiguous 1 KB run per instruction, and k_agg3's TMA
 // still reads 64-byte runs of one label (16 pixels) per request.
 constexpr int kWGroupPx = 16, kWGroupLabels = 32;
+// Suspend-time hint (ns) for mbarrier.try_wait: a waiting warp is parked until the phase completes (or
+// the hint elapses) instead of spinning through issue slots the working warps need.
+constexpr unsigned kMbarSuspendNs = 20000;
 // Floats per pixel record of the per-pixel ("AoS") statistics layout read by k_coef3.
 constexpr int kStatsAos = 28;
 struct WLayout {

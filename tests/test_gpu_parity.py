@@ -175,9 +175,10 @@ def test_invalid_arguments_fail_loudly():
         h.aggregate_wta(torch.zeros(3, 10, 10, device="cuda"), torch.zeros(2, 10, 11, device="cuda"))
 
 
-@pytest.mark.parametrize("kernel_env,val", [("HGF_COEF3", "0"), ("HGF_NO_V3", "1"), ("HGF_FORCE_V1", "1")])
+@pytest.mark.parametrize("kernel_env,val", [("HGF_COEF3", "0"), ("HGF_NO_V3", "1"), ("HGF_FORCE_V1", "1"),
+                                             ("HGF_COEF4", "1")])
 def test_kernel_variants_parity(monkeypatch, kernel_env, val):
-    """Every coefficient/aggregation kernel variant against the oracle (k_coef2, v2 flat layout, v1)."""
+    """Every coefficient/aggregation kernel variant against the oracle (k_coef2, v2 flat layout, v1, k_coef4)."""
     monkeypatch.setenv(kernel_env, val)
     c = synth.config("C2")
     scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
@@ -185,6 +186,22 @@ def test_kernel_variants_parity(monkeypatch, kernel_env, val):
     I = np.ascontiguousarray(scene.left[:, :200, :260])
     res = _run(I, V, c["d"], c["r"], c["lam"])
     Z = O.hgf_filter(I, V, c["lam"], c["r"], c["d"])
+    s_v = float(np.abs(V).max())
+    check_z(res["filtered"], Z, s_v)
+    check_labels(res["labels"], Z, s_v)
+
+
+@pytest.mark.parametrize("r,mode,m,d", [(9, "hgf", 3, 2), (4, "gf", 3, 2), (2, "hgf", 3, 1), (7, "gf", 1, 3),
+                                       (1, "hgf", 1, 1)])
+def test_coef4_tensor_core_parity(monkeypatch, r, mode, m, d):
+    """k_coef4 (tcgen05 horizontal sums): radii 1..9, both modes, n = 1..6, a ragged third strip, 20 labels."""
+    monkeypatch.setenv("HGF_COEF4", "1")
+    W, H, L = 292, 61, 20
+    scene = synth.make_stereo_scene(W, H, L, seed=40 + r)
+    I = scene.left if m == 3 else synth.smooth_guides(W, H, m, seed=41)
+    V = synth.stereo_cost_volume_np(scene, L)
+    res = _run(np.ascontiguousarray(I), V, d, r, 0.05, mode)
+    Z = O.hgf_filter(I, V, 0.05, r, d, mode=mode)
     s_v = float(np.abs(V).max())
     check_z(res["filtered"], Z, s_v)
     check_labels(res["labels"], Z, s_v)
