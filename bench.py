@@ -185,7 +185,8 @@ def run_reference(args, c):
 def config_json(c, n_gpus):
     return {"workload": workload_name(c), "W": c["W"], "H": c["H"], "labels": c["L"], "n_guide": c["m"],
             "poly_degree": c["d"], "n": c["n"], "radius": c["r"], "lambda": c["lam"],
-            "parallelism": f"label-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
+            "parallelism": (f"labels sharded x{n_gpus} (keys allreduce-MIN), statistics rows sharded (all-gather)"
+                            if n_gpus > 1 else "single GPU"),
             "l2": "inputs larger than L2 (cost volume > 126 MB); no flush needed"}
 
 
@@ -201,7 +202,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1803_00005_b200 import HGF, merge_keys_allreduce, shard_range
+    from paper_1803_00005_b200 import HGF, HGFError, gather_stats_rows, merge_keys_allreduce, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,9 +224,26 @@ def main():
     keys = torch.empty((H, W), dtype=torch.int64, device=dev)
     mincost = torch.empty((H, W), dtype=torch.float32, device=dev)
 
+    # N > 1: statistics row-sharded (each rank its band of rows, NCCL all-gather), slices label-sharded,
+    # WTA merged by the int64 allreduce-MIN of packed keys
+    y0, y1 = shard_range(H, world, rank)
+    row_sharded = False
+    if world > 1:
+        try:
+            h.stats_view()
+            row_sharded = True
+        except HGFError:
+            row_sharded = False
+
     def step():
         if world == 1:
             h.aggregate_wta(guide, vol, labels)
+        elif row_sharded:
+            h.prepare_rows(guide, y0, y1)
+            gather_stats_rows(h)
+            h.aggregate_wta_prepared(vol, label_offset=l0, labels=False, keys=True, out={"keys": keys})
+            merge_keys_allreduce(keys)
+            h.unpack_keys(keys, labels, mincost)
         else:
             h.aggregate_wta_ex(guide, vol, label_offset=l0, labels=False, keys=True, out={"keys": keys})
             merge_keys_allreduce(keys)
@@ -342,7 +360,9 @@ def main():
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
             e2e = {"value": W * H * L * args.e2e_steps / float(dt.item()), "unit": UNIT,
                    "h2d_bytes_per_step": 4 * W * H * L + 4 * m * W * H * world, "d2h_bytes_per_step": 4 * W * H,
-                   "api": "torch H2D copies + HGF.aggregate_wta_ex + NCCL allreduce-MIN + HGF.unpack_keys"}
+                   "api": ("torch H2D copies + HGF.prepare_rows + NCCL all-gather of the statistics rows + "
+                           "HGF.aggregate_wta_prepared + NCCL allreduce-MIN + HGF.unpack_keys" if row_sharded else
+                           "torch H2D copies + HGF.aggregate_wta_ex + NCCL allreduce-MIN + HGF.unpack_keys")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -112,6 +112,28 @@ HGF_API hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const 
                                 int label_offset, int32_t* labels_out, float* min_cost_out,
                                 float* filtered_out, int64_t* keys_out);
 
+/* Row-sharded frame preparation.  Steps 1-2 of the path for a row band:
+ * the polynomial guidance for the whole frame (cheap, needed by every slice kernel) and the
+ * label-independent statistics (Prop 1 recursion, Eq4 P:143-151 with readings F1/F2) of image rows
+ * [y0, y1) only, 0 <= y0 <= y1 <= H.  Rows outside the band keep the buffer's previous contents: the caller
+ * fills them, e.g. by an all-gather of every rank's band (hgf_stats_buffer), before
+ * hgf_aggregate_wta_prepared.  guide: device, [n_guide][H][W] f32.  HGF_ERR_UNSUPPORTED unless the
+ * configuration uses the per-pixel statistics layout of the k_coef3/k_coef4 path (n <= 6, W % 4 == 0,
+ * r <= 9 and a TMA-capable device); the unsharded entry points always work. */
+HGF_API hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1);
+
+/* The device statistics buffer written by hgf_prepare_rows: H rows of *bytes_per_row bytes each, row y at
+ * dev_ptr + y * bytes_per_row (owned by the handle; valid until hgf_destroy).  HGF_ERR_UNSUPPORTED as
+ * above. */
+HGF_API hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row);
+
+/* hgf_aggregate_wta_ex without steps 1-2: the slices use the guidance and statistics already in the
+ * handle (from hgf_prepare_rows; every row must be filled).  Arguments, outputs and errors as
+ * hgf_aggregate_wta_ex. */
+HGF_API hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, int L, int label_offset,
+                                              int32_t* labels_out, float* min_cost_out, float* filtered_out,
+                                              int64_t* keys_out);
+
 /* Unpack merged (signed) keys [H][W] into labels_out (int32, may be NULL) and min_cost_out (float, may be NULL). */
 HGF_API hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_out, float* min_cost_out);
 

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 __all__ = ["HGF", "HGFError", "lib", "lib_path", "MODE_HGF", "MODE_GF", "EXPORTED_SYMBOLS",
-           "merge_keys_allreduce", "shard_range"]
+           "merge_keys_allreduce", "shard_range", "gather_stats_rows"]
 
 MODE_HGF = 0
 MODE_GF = 1
@@ -23,6 +23,7 @@ EXPORTED_SYMBOLS = (
     "hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter",
     "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
     "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
+    "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared",
 )
 KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys")   # HGF_KC_* order
 
@@ -61,8 +62,12 @@ def lib():
     L.hgf_set_profiling.restype = c_int
     L.hgf_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int), c_int]
     L.hgf_profile_read.restype = c_int
+    L.hgf_prepare_rows.argtypes = [vp, vp, c_int, c_int]
+    L.hgf_stats_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
+    L.hgf_aggregate_wta_prepared.argtypes = [vp, vp, c_int, c_int, vp, vp, vp, vp]
     for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
-                 "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host"):
+                 "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host", "hgf_prepare_rows",
+                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -152,13 +157,8 @@ class HGF:
                     "hgf_aggregate_wta")
         return labels_out
 
-    def aggregate_wta_ex(self, guide, cost_volume, label_offset=0, labels=True, min_cost=False, filtered=False,
-                         keys=False, out=None):
-        """Returns a dict with the requested outputs ('labels', 'min_cost', 'filtered', 'keys')."""
+    def _outputs(self, L, labels, min_cost, filtered, keys, out):
         torch = self._torch
-        L = cost_volume.shape[0]
-        self._dev(guide, (self.m, self.H, self.W), torch.float32, "guide")
-        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
         out = dict(out or {})
         dev, HW = self.device, (self.H, self.W)
         if labels and "labels" not in out:
@@ -177,11 +177,52 @@ class HGF:
             self._dev(out["filtered"], (L,) + HW, torch.float32, "filtered")
         if "keys" in out:
             self._dev(out["keys"], HW, torch.int64, "keys")
+        return out
+
+    def aggregate_wta_ex(self, guide, cost_volume, label_offset=0, labels=True, min_cost=False, filtered=False,
+                         keys=False, out=None):
+        """Returns a dict with the requested outputs ('labels', 'min_cost', 'filtered', 'keys')."""
+        torch = self._torch
+        L = cost_volume.shape[0]
+        self._dev(guide, (self.m, self.H, self.W), torch.float32, "guide")
+        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
+        out = self._outputs(L, labels, min_cost, filtered, keys, out)
         self._bind_stream()
         self._check(lib().hgf_aggregate_wta_ex(self._h, _ptr(guide), _ptr(cost_volume), L, int(label_offset),
                                                _ptr(out.get("labels")), _ptr(out.get("min_cost")),
                                                _ptr(out.get("filtered")), _ptr(out.get("keys"))),
                     "hgf_aggregate_wta_ex")
+        return out
+
+    def prepare_rows(self, guide, y0, y1):
+        """hgf_prepare_rows: guidance for the frame + statistics of rows [y0, y1)."""
+        self._dev(guide, (self.m, self.H, self.W), self._torch.float32, "guide")
+        self._bind_stream()
+        self._check(lib().hgf_prepare_rows(self._h, _ptr(guide), int(y0), int(y1)), "hgf_prepare_rows")
+
+    def stats_view(self):
+        """hgf_stats_buffer as a float32 tensor view (H, bytes_per_row / 4) on the handle's device (no copy;
+        valid while the handle lives)."""
+        p, bpr = ctypes.c_void_p(), ctypes.c_size_t()
+        self._check(lib().hgf_stats_buffer(self._h, ctypes.byref(p), ctypes.byref(bpr)), "hgf_stats_buffer")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (self.H, bpr.value // 4), "typestr": "<f4",
+                                        "data": (p.value, False), "version": 3, "strides": None}
+        return self._torch.as_tensor(_View(), device=self.device)
+
+    def aggregate_wta_prepared(self, cost_volume, label_offset=0, labels=True, min_cost=False, filtered=False,
+                               keys=False, out=None):
+        """hgf_aggregate_wta_prepared (statistics from prepare_rows); returns the requested outputs."""
+        torch = self._torch
+        L = cost_volume.shape[0]
+        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
+        out = self._outputs(L, labels, min_cost, filtered, keys, out)
+        self._bind_stream()
+        self._check(lib().hgf_aggregate_wta_prepared(self._h, _ptr(cost_volume), L, int(label_offset),
+                                                     _ptr(out.get("labels")), _ptr(out.get("min_cost")),
+                                                     _ptr(out.get("filtered")), _ptr(out.get("keys"))),
+                    "hgf_aggregate_wta_prepared")
         return out
 
     def unpack_keys(self, keys, labels_out=None, min_cost_out=None):
@@ -235,3 +276,22 @@ def merge_keys_allreduce(keys, group=None):
     import torch.distributed as dist
     dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
     return keys
+
+
+def gather_stats_rows(h, group=None):
+    """Row-sharded statistics: every rank computes the statistics of its band of rows
+    (shard_range over H) with ``h.prepare_rows`` beforehand; this all-gathers the bands into every rank's
+    statistics buffer (in place; NCCL all-gather when the bands are equal, else one broadcast per rank)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    view = h.stats_view()
+    bands = [shard_range(h.H, world, r) for r in range(world)]
+    if h.H % world == 0:
+        y0, y1 = bands[rank]
+        dist.all_gather_into_tensor(view, view[y0:y1], group=group)
+    else:
+        for src, (y0, y1) in enumerate(bands):
+            g_src = src if group is None else dist.get_global_rank(group, src)
+            dist.broadcast(view[y0:y1].contiguous() if not view[y0:y1].is_contiguous() else view[y0:y1], src=g_src,
+                           group=group)
+    return view

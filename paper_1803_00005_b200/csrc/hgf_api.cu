@@ -136,7 +136,8 @@ hgf_status check_async(hgf_ctx* h) {
 }
 
 // Steps 1-2: guidance + label-independent statistics (once per frame).
-hgf_status frame_stats(hgf_ctx* h, const float* guide) {
+// Steps 1-2: polynomial guidance (all rows) and the statistics of rows [y0, y1).
+hgf_status frame_stats(hgf_ctx* h, const float* guide, int y0, int y1) {
   cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
     return hgf::launch_poly_guidance(guide, h->G, h->m, h->d, h->W, h->H, h->stream);
   });
@@ -144,8 +145,7 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide) {
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
     const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
     return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode,
-                             (h->v3coef || h->v4coef) ? 1 : 0, lam0,
-                             h->stream);
+                             (h->v3coef || h->v4coef) ? 1 : 0, lam0, y0, y1, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
   return HGF_OK;
@@ -410,7 +410,7 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
   if (dst == src || dst == guide) return fail(h, HGF_ERR_INVALID_ARGUMENT, "dst aliases an input");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
-  if ((s = frame_stats(h, guide)) != HGF_OK) return s;
+  if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   return slices(h, guide, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
 }
 
@@ -427,9 +427,50 @@ hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* c
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
-  if ((s = frame_stats(h, guide)) != HGF_OK) return s;
+  if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
   return slices(h, guide, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
+}
+
+hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!guide) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null guide");
+  if (y0 < 0 || y1 > h->H || y0 > y1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "row band out of range");
+  if (!(h->v3coef || h->v4coef))
+    return fail(h, HGF_ERR_UNSUPPORTED, "row-band statistics need the per-pixel statistics layout (n <= 6, W % 4 == 0)");
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  return frame_stats(h, guide, y0, y1);
+}
+
+hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row) {
+  if (!h || !dev_ptr || !bytes_per_row) return HGF_ERR_INVALID_ARGUMENT;
+  if (!(h->v3coef || h->v4coef))
+    return fail(h, HGF_ERR_UNSUPPORTED, "statistics are not stored row-contiguously in this configuration");
+  *dev_ptr = h->stats;
+  *bytes_per_row = sizeof(float) * (size_t)hgf::kStatsAos * h->W;
+  return HGF_OK;
+}
+
+hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, int L, int label_offset,
+                                      int32_t* labels_out, float* min_cost_out, float* filtered_out,
+                                      int64_t* keys_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!cost_volume) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null input pointer");
+  if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
+  if (label_offset < 0 || (long long)label_offset + L > 2147483647LL)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
+  if (!labels_out && !min_cost_out && !filtered_out && !keys_out)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
+  if (!(h->v3coef || h->v4coef)) return fail(h, HGF_ERR_UNSUPPORTED, "prepared statistics need the k_coef3/4 path");
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
+  return slices(h, nullptr, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {
@@ -477,7 +518,7 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
   if ((e = cudaMemcpyAsync(h->st_guide, guide_host, sizeof(float) * h->m * HW, cudaMemcpyHostToDevice, h->stream)) !=
       cudaSuccess)
     return cuda_fail(h, e, "guide H2D");
-  if ((s = frame_stats(h, h->st_guide)) != HGF_OK) return s;
+  if ((s = frame_stats(h, h->st_guide, 0, h->H)) != HGF_OK) return s;
   const long long lcap = h->st_chunk;
   const int nchunks = (int)((L + lcap - 1) / lcap);
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;

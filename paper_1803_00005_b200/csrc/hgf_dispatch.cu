@@ -54,18 +54,18 @@ cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, 
   }
 
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
-                         float lam0f, cudaStream_t st) {
+                         float lam0f, int y0, int y1, cudaStream_t st) {
   // sliding-sum version when all n+1 channel tiles fit in shared memory, else the pairwise v1 kernel
   const int TS = 16 + 2 * r;
   // = st2::smem_bytes(n, r): odd-pitch channel tiles, 17-double rows of horizontal sums, vertical sums
   const size_t smem2 = ((size_t)(n + 1) * TS * (TS | 1) * 4 + 15) / 16 * 16 + (size_t)8 * TS * 17 * 8 +
                        (size_t)8 * 16 * 16 * 8 + 16;
   if (smem2 <= 200 * 1024) {
-#define CALL(N) st2::stats2_impl<N>(G, stats, W, H, r, lam, mode, aos, lam0f, st)
+#define CALL(N) st2::stats2_impl<N>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st)
     HGF_DISPATCH(n, CALL)
 #undef CALL
   }
-  if (aos) return cudaErrorInvalidValue;
+  if (aos || y0 != 0 || y1 != H) return cudaErrorInvalidValue;
 #define CALL(N) stats_impl<N>(G, stats, W, H, r, lam, mode, st)
   HGF_DISPATCH(n, CALL)
 #undef CALL

@@ -58,6 +58,7 @@ void agg3_box(int R, int il, int* bx, int* by) {
 #include "hgf_stats_v2.cuh"
 namespace hgf {
 namespace st2 {
-template cudaError_t stats2_impl<HGF_N>(const float*, float*, int, int, int, double, int, int, float, cudaStream_t);
+template cudaError_t stats2_impl<HGF_N>(const float*, float*, int, int, int, double, int, int, float, int, int,
+                                        cudaStream_t);
 }  // namespace st2
 }  // namespace hgf

@@ -25,8 +25,9 @@ struct AggArgs {
 cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st);
 // aos = 1: per-pixel records of kStatsAos floats (statistics, then kappa = 1/(lam0f + N)) for k_coef3;
 // needs the k_stats2 path (else cudaErrorInvalidValue).
+// Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
-                         float lam0f, cudaStream_t st);
+                         float lam0f, int y0, int y1, cudaStream_t st);
 cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H,
                         int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st);
@@ -98,6 +99,6 @@ namespace hgf {
 namespace st2 {
 template <int NC>
 cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
-                        cudaStream_t st);
+                        int y0, int y1, cudaStream_t st);
 }  // namespace st2
 }  // namespace hgf

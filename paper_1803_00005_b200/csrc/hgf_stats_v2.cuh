@@ -31,9 +31,11 @@ __host__ __device__ inline size_t smem_bytes(int NC, int r) {
          (size_t)PB * T * T * 8 + 16;
 }
 
+// Rows [yb0, yb1) only (tiles from row yb0 & ~15; rows outside the band are not written).
 template <int NC>
 __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G, float* __restrict__ stats, int W,
-                                                    int H, int r, double lam, int mode, int aos, float lam0f) {
+                                                    int H, int r, double lam, int mode, int aos, float lam0f,
+                                                    int yb0, int yb1) {
   constexpr int K = NC + 1;
   constexpr int NPAIR = K * (K + 1) / 2 - 1;     // (0,0) is N_p, analytic
   constexpr int NB = (NPAIR + PB - 1) / PB;
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
   double* vb = hb + PB * TS * HP;                                                 // [PB][T][T]
   const int tid = threadIdx.x;
   const int tx = tid % T, ty = tid / T;
-  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
+  const int x0 = blockIdx.x * T, y0 = (yb0 / T + (int)blockIdx.y) * T;
   const long long HW = (long long)H * W;
 
   for (int e = tid; e < K * TS * TS; e += THREADS) {
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
       if (bt * PB + pb < NPAIR) g[bt * PB + pb] = vb[(pb * T + ty) * T + tx];
   }
   const int gx = x0 + tx, gy = y0 + ty;
-  if (gx >= W || gy >= H) return;
+  if (gx >= W || gy >= H || gy < yb0 || gy >= yb1) return;
   const double N = (double)window_count(gy, gx, H, W, r);
   double Gm[K][K];
 #pragma unroll
@@ -185,13 +187,14 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
 
 template <int NC>
 cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
-                        cudaStream_t st) {
+                        int y0, int y1, cudaStream_t st) {
   if (aos && stats_planes(NC) + 1 > kStatsAos) return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(NC, r);
   cudaError_t e = cudaFuncSetAttribute(k_stats2<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((W + T - 1) / T, (H + T - 1) / T);
-  k_stats2<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f);
+  if (y0 >= y1) return cudaSuccess;
+  dim3 grid((W + T - 1) / T, (y1 + T - 1) / T - y0 / T);
+  k_stats2<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1);
   return cudaGetLastError();
 }
 

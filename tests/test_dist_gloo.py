@@ -67,3 +67,38 @@ def test_shard_range_partition():
             assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
             sizes = [b - a for a, b in ranges]
             assert max(sizes) - min(sizes) <= 1
+
+
+class _FakeHandle:
+    """Stands in for HGF in gather_stats_rows: H rows, a CPU statistics buffer (the real one is on the GPU)."""
+
+    def __init__(self, H, C):
+        self.H = H
+        self.buf = torch.full((H, C), float("nan"))
+
+    def stats_view(self):
+        return self.buf
+
+
+def _stats_worker(rank, world, port, H, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1803_00005_b200 import gather_stats_rows, shard_range
+    h = _FakeHandle(H, 6)
+    y0, y1 = shard_range(H, world, rank)
+    rows = torch.arange(H, dtype=torch.float32)[:, None] * 10 + torch.arange(6, dtype=torch.float32)[None, :]
+    h.buf[y0:y1] = rows[y0:y1]                       # this rank's band only (prepare_rows on the GPU)
+    gather_stats_rows(h)
+    torch.save(h.buf, out_path + f".{rank}")
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("H", [8, 7])                 # equal bands (all-gather) and unequal (broadcasts)
+def test_gloo_world2_row_sharded_statistics(tmp_path, H):
+    world = 2
+    out = str(tmp_path / "stats")
+    mp.spawn(_stats_worker, args=(world, _free_port(), H, out), nprocs=world, join=True)
+    rows = torch.arange(H, dtype=torch.float32)[:, None] * 10 + torch.arange(6, dtype=torch.float32)[None, :]
+    for r in range(world):
+        assert torch.equal(torch.load(out + f".{r}"), rows)

@@ -205,3 +205,38 @@ def test_coef4_tensor_core_parity(monkeypatch, r, mode, m, d):
     s_v = float(np.abs(V).max())
     check_z(res["filtered"], Z, s_v)
     check_labels(res["labels"], Z, s_v)
+
+
+@pytest.mark.parametrize("coef4", ["0", "1"])
+def test_prepared_row_bands_equal_unsharded(monkeypatch, coef4):
+    """Row-sharded statistics (hgf_prepare_rows per band + hgf_aggregate_wta_prepared) == the one-call path,
+    bit-exactly; bands of unequal height, as uneven rank counts produce."""
+    torch = _torch()
+    monkeypatch.setenv("HGF_COEF4", coef4)
+    c = synth.config("C2")
+    scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
+    V = synth.stereo_cost_volume_np(scene, 40)[:, :200, :260].copy()
+    I = np.ascontiguousarray(scene.left[:, :200, :260])
+    ref = _run(I, V, c["d"], c["r"], c["lam"])
+    h = _hgf(260, 200, 3, c["d"], c["r"], c["lam"], "hgf")
+    gi, gv = torch.from_numpy(I).cuda(), torch.from_numpy(V).cuda()
+    view = h.stats_view()
+    view.fill_(float("nan"))                              # every row must come from some band
+    for y0, y1 in ((0, 70), (70, 151), (151, 200)):
+        h.prepare_rows(gi, y0, y1)
+    out = h.aggregate_wta_prepared(gv, labels=True, min_cost=True, filtered=True, keys=True)
+    torch.cuda.synchronize()
+    for k in ("filtered", "labels", "min_cost", "keys"):
+        assert np.array_equal(out[k].cpu().numpy(), ref[k]), k
+    h.close()
+
+
+def test_prepared_path_unsupported_config_fails_loudly():
+    torch = _torch()
+    from paper_1803_00005_b200 import HGFError
+    h = _hgf(40, 30, 3, 3, 4, 0.05, "hgf")                  # n = 9: planar statistics, no row bands
+    with pytest.raises(HGFError):
+        h.prepare_rows(torch.zeros(3, 30, 40, device="cuda"), 0, 30)
+    with pytest.raises(HGFError):
+        h.stats_view()
+    h.close()
