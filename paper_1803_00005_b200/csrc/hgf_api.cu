@@ -99,7 +99,7 @@ size_t coef_budget_bytes() {
     return (size_t)(mb < 1 ? 1 : mb) << 20;
   }
   size_t fr = 0, tot = 0;
-  size_t budget = (size_t)16 << 30;
+  size_t budget = (size_t)32 << 30;   // <= 40 % of free memory; fewer, larger chunks shorten kernel tails
   if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr / 10 * 4 < budget) budget = fr / 10 * 4;
   return budget < ((size_t)64 << 20) ? ((size_t)64 << 20) : budget;
 }
@@ -258,8 +258,13 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
 hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
                   int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
   const long long HW = (long long)h->W * h->H;
-  for (int c0 = 0; c0 < L; c0 += h->lcap) {
-    const int Lc = (L - c0 < h->lcap) ? (L - c0) : h->lcap;
+  // balanced chunks (e.g. 256 labels with a 147-label capacity -> 2 x 128, not 128 + 128 + ... tails)
+  const int nchunks = (L + h->lcap - 1) / h->lcap;
+  int step = (L + nchunks - 1) / nchunks;
+  step = (step + hgf::kWGroupLabels - 1) / hgf::kWGroupLabels * hgf::kWGroupLabels;
+  if (step > h->lcap) step = h->lcap;
+  for (int c0 = 0; c0 < L; c0 += step) {
+    const int Lc = (L - c0 < step) ? (L - c0) : step;
     cudaError_t e = launch_coef_chunk(h, guide, vol + (long long)c0 * HW, Lc);
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
