@@ -36,6 +36,7 @@ __all__ = [
     "poly_guidance", "gram_planes", "alpha_recursion", "weights_eq13",
     "hgf_filter", "hgf_filter_brute", "gf_he",
     "wta", "aggregate_wta", "pack_keys", "unpack_keys",
+    "stereo_cost", "stereo_cost_brute",
 ]
 
 MODE_HGF = "hgf"
@@ -374,3 +375,74 @@ def unpack_keys(keys: np.ndarray):
     hi = (o >> np.uint64(31)) & np.uint64(1)
     b = np.where(hi == 1, o & np.uint64(0x7FFFFFFF), (~o) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     return b.view(np.float32), (keys & np.uint64(0xFFFFFFFF)).astype(np.int32)
+
+
+# ----------------------------------------------------------------------------- stereo cost
+def _gray_grad_x(img: np.ndarray) -> np.ndarray:
+    """d/dx of the channel mean: central difference inside, one-sided at the two border columns."""
+    g = img.astype(np.float64).mean(axis=0)
+    out = np.empty_like(g)
+    if g.shape[1] == 1:
+        out[:] = 0.0
+        return out
+    out[:, 1:-1] = 0.5 * (g[:, 2:] - g[:, :-2])
+    out[:, 0] = g[:, 1] - g[:, 0]
+    out[:, -1] = g[:, -1] - g[:, -2]
+    return out
+
+
+def stereo_cost(left: np.ndarray, right: np.ndarray, L: int, l0: int = 0, alpha: float = 0.11,
+                tau_c: float = 0.028, tau_g: float = 0.008) -> np.ndarray:
+    """Truncated colour + gradient matching cost of disparity d = l0 .. l0+L-1 (the paper defers the stereo
+    cost to Hosni et al.; the form here is SPEC S:400):
+
+        C(x, y, d) = alpha min(mean_c |L_c(x,y) - R_c(x-d,y)|, tau_c) + (1-alpha) min(|dx L~ - dx R~(x-d)|, tau_g)
+
+    with L~ / R~ the channel means and dx the central x-difference (one-sided at the borders); pixels with
+    x - d < 0 take the truncation value alpha tau_c + (1-alpha) tau_g.  float64, (L, H, W)."""
+    left = left.astype(np.float64)
+    right = right.astype(np.float64)
+    _, H, W = left.shape
+    gl, gr = _gray_grad_x(left), _gray_grad_x(right)
+    trunc = alpha * tau_c + (1.0 - alpha) * tau_g
+    out = np.full((L, H, W), trunc)
+    for k in range(L):
+        d = l0 + k
+        if d >= W:
+            continue
+        col = np.abs(left[:, :, d:] - right[:, :, :W - d]).mean(axis=0)
+        grd = np.abs(gl[:, d:] - gr[:, :W - d])
+        out[k, :, d:] = alpha * np.minimum(col, tau_c) + (1.0 - alpha) * np.minimum(grd, tau_g)
+    return out
+
+
+def stereo_cost_brute(left: np.ndarray, right: np.ndarray, L: int, l0: int = 0, alpha: float = 0.11,
+                      tau_c: float = 0.028, tau_g: float = 0.008) -> np.ndarray:
+    """stereo_cost by explicit per-pixel loops (tiny inputs only; pins the vectorised form)."""
+    m, H, W = left.shape
+
+    def gray(img, y, x):
+        return sum(float(img[c, y, x]) for c in range(m)) / m
+
+    def gx(img, y, x):
+        if W == 1:
+            return 0.0
+        if x == 0:
+            return gray(img, y, 1) - gray(img, y, 0)
+        if x == W - 1:
+            return gray(img, y, W - 1) - gray(img, y, W - 2)
+        return 0.5 * (gray(img, y, x + 1) - gray(img, y, x - 1))
+
+    out = np.empty((L, H, W))
+    for k in range(L):
+        d = l0 + k
+        for y in range(H):
+            for x in range(W):
+                if x - d < 0:
+                    out[k, y, x] = alpha * tau_c + (1 - alpha) * tau_g
+                    continue
+                col = sum(abs(float(left[c, y, x]) - float(right[c, y, x - d])) for c in range(m)) / m
+                grd = abs(gx(left, y, x) - gx(right, y, x - d))
+                out[k, y, x] = alpha * min(col, tau_c) + (1 - alpha) * min(grd, tau_g)
+    return out
+

@@ -297,3 +297,48 @@ def test_keys_order_and_roundtrip():
     full = O.pack_keys(V.min(0), V.argmin(0))
     shards = [O.pack_keys(V[a:b].min(0), a + V[a:b].argmin(0)) for a, b in [(0, 3), (3, 5), (5, 8)]]
     assert np.array_equal(np.minimum.reduce(shards), full)
+
+
+# ----------------------------------------------------------------------------- stereo cost (NEXT-2)
+def test_stereo_cost_matches_brute_force_and_edge_cases():
+    rng = np.random.default_rng(3)
+    left = rng.random((3, 5, 9))
+    right = rng.random((3, 5, 9))
+    a = O.stereo_cost(left, right, 6, l0=1)
+    b = O.stereo_cost_brute(left, right, 6, l0=1)
+    assert np.allclose(a, b, rtol=0, atol=1e-15)
+    trunc = 0.11 * 0.028 + 0.89 * 0.008
+    assert np.all(a[:, :, 0] == trunc)                     # x - d < 0 for every d >= 1 at x = 0
+    assert np.all(a[4] [:, :5] == trunc)                    # d = 5: columns 0..4 out of range
+    # identical views at d = 0: zero colour and gradient terms
+    z = O.stereo_cost(left, left, 1)
+    assert np.all(z == 0.0)
+    # a view shifted by exactly s pixels matches at d = s away from the border columns
+    s = 2
+    shifted = np.zeros_like(left)
+    shifted[:, :, :9 - s] = left[:, :, s:]
+    c = O.stereo_cost(left, shifted, 4)
+    assert np.allclose(c[s][:, s + 1:-1], 0.0, atol=1e-15)
+
+
+def test_stereo_cost_truncation_bounds_and_weights():
+    rng = np.random.default_rng(4)
+    left, right = rng.random((3, 6, 11)), rng.random((3, 6, 11))
+    c = O.stereo_cost(left, right, 5, alpha=0.3, tau_c=0.1, tau_g=0.05)
+    assert c.min() >= 0.0 and c.max() <= 0.3 * 0.1 + 0.7 * 0.05 + 1e-15
+    # untruncated regime: huge thresholds give exactly alpha*colour + (1-alpha)*gradient
+    big = O.stereo_cost(left, right, 3, alpha=0.25, tau_c=1e9, tau_g=1e9)
+    col = np.abs(left[:, :, 2:] - right[:, :, :-2]).mean(axis=0)
+    gl, gr = np.gradient(left.mean(axis=0), axis=1), np.gradient(right.mean(axis=0), axis=1)   # same stencil
+    g = gl[:, 2:] - gr[:, :-2]
+    assert np.allclose(big[2][:, 2:], 0.25 * col + 0.75 * np.abs(g), rtol=0, atol=1e-14)
+
+
+def test_stereo_cost_agrees_with_the_workload_generator():
+    """Two independent implementations of S:400: the oracle (float64) and synth's input generator (float32)."""
+    import synth
+    scene = synth.make_stereo_scene(40, 24, 12, seed=9)
+    gen = synth.stereo_cost_volume_np(scene, 12)
+    ora = O.stereo_cost(scene.left, scene.right, 12)
+    # the generator works in float32 on [0, 1] intensities: a few ulps (6e-8) of the gradient terms
+    assert np.abs(gen - ora).max() < 3e-7
