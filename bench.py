@@ -190,6 +190,40 @@ def config_json(c, n_gpus):
             "l2": "inputs larger than L2 (cost volume > 126 MB); no flush needed"}
 
 
+def stereo_leg(h, scene, L, W, H, args, torch):
+    """NEXT-2 (hgf_stereo_wta): the same voxels aggregated + WTA, with the cost slices built on the GPU from
+    the two views; device throughput and end to end from pinned host views (only 2 x 3 x H x W floats in)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    left_h = torch.from_numpy(scene.left).pin_memory()
+    right_h = torch.from_numpy(scene.right).pin_memory()
+    left, right = left_h.to(dev), right_h.to(dev)
+    lab = torch.empty((H, W), dtype=torch.int32, device=dev)
+    lab_h = torch.empty((H, W), dtype=torch.int32, pin_memory=True)
+    for _ in range(max(1, args.warmup)):
+        h.stereo_wta(left, right, L, out={"labels": lab})
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        h.stereo_wta(left, right, L, out={"labels": lab})
+    e1.record(st)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / args.steps
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        left.copy_(left_h, non_blocking=True)
+        right.copy_(right_h, non_blocking=True)
+        h.stereo_wta(left, right, L, out={"labels": lab})
+        lab_h.copy_(lab, non_blocking=True)
+        torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    return {"value": W * H * L / (dev_ms / 1e3), "ms_per_step": dev_ms, "unit": UNIT,
+            "e2e": {"value": W * H * L / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * left_h.numel() * 4,
+                    "d2h_bytes_per_step": lab_h.numel() * 4},
+            "api": "hgf_stereo_wta (SURVEY 8(f) NEXT-2: S:400 cost slices built per chunk on the GPU)"}
+
+
 # ----------------------------------------------------------------------------- own arm
 def main():
     args = parse()
@@ -321,6 +355,7 @@ def main():
 
     # e2e through the public API with host buffers
     e2e = None
+    stereo = None
     if not args.no_e2e:
         if world == 1:
             vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
@@ -337,6 +372,7 @@ def main():
                    "h2d_bytes_per_step": vol_h.numel() * 4 + guide_h.numel() * 4, "d2h_bytes_per_step": lab_h.numel() * 4,
                    "api": "hgf_aggregate_wta_host (chunked H2D overlapped with compute)"}
             del vol_h
+            stereo = stereo_leg(h, scene, L, W, H, args, torch)
         else:
             vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
             vol_h.copy_(vol)
@@ -377,7 +413,7 @@ def main():
                 "config": config_json(c, world), "roofline": roofline,
                 "hbm": {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
                         "alg_bytes_per_step": alg_bytes(W, H, L, m)},
-                "stage_ms_per_step": stage_ms, "cpu_baseline": cpu, "e2e": e2e,
+                "stage_ms_per_step": stage_ms, "cpu_baseline": cpu, "e2e": e2e, "stereo_cost_on_gpu": stereo,
                 "gpu_launches": int(lt.item()), "clocks": clk}
         print(json.dumps(line), flush=True)
     h.close()

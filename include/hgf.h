@@ -112,6 +112,21 @@ HGF_API hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const 
                                 int label_offset, int32_t* labels_out, float* min_cost_out,
                                 float* filtered_out, int64_t* keys_out);
 
+/* Stereo aggregation with the cost volume built on the GPU.  The label slices are the
+ * matching costs of disparities d = label_offset .. label_offset + L - 1 between the two views (the paper
+ * defers the cost to Hosni et al.; the form is SPEC S:400):
+ *   C(x,y,d) = alpha min(mean_c |L_c(x,y) - R_c(x-d,y)|, tau_color)
+ *            + (1 - alpha) min(|dx Lbar(x,y) - dx Rbar(x-d,y)|, tau_grad),
+ * Lbar/Rbar the channel means, dx the central x-difference (one-sided at the border columns), x - d < 0 ->
+ * alpha tau_color + (1 - alpha) tau_grad; then steps 1-4 exactly as hgf_aggregate_wta_ex with the left view
+ * as the guide.  left, right: device [3][H][W] f32 (the handle must have n_guide = 3).  Only the chunk being
+ * filtered is materialised (library scratch, allocated on first use).  Outputs as hgf_aggregate_wta_ex;
+ * HGF_ERR_INVALID_ARGUMENT for null views, n_guide != 3, alpha outside [0,1] or negative/non-finite
+ * thresholds. */
+HGF_API hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, int L, int label_offset,
+                                  float alpha, float tau_color, float tau_grad, int32_t* labels_out,
+                                  float* min_cost_out, float* filtered_out, int64_t* keys_out);
+
 /* Row-sharded frame preparation.  Steps 1-2 of the path for a row band:
  * the polynomial guidance for the whole frame (cheap, needed by every slice kernel) and the
  * label-independent statistics (Prop 1 recursion, Eq4 P:143-151 with readings F1/F2) of image rows
@@ -152,7 +167,8 @@ enum {
   HGF_KC_COEF = 2,     /* K4a per-slice coefficients w           */
   HGF_KC_AGG = 3,      /* K4b per-slice aggregation Z + WTA      */
   HGF_KC_KEYS = 4,     /* key unpacking                          */
-  HGF_KC_COUNT = 5
+  HGF_KC_COST = 5,     /* stereo cost construction (hgf_stereo_wta) */
+  HGF_KC_COUNT = 6
 };
 
 /* Tracing: when enable != 0, every kernel launch of this handle is bracketed by CUDA events recorded

@@ -23,9 +23,9 @@ EXPORTED_SYMBOLS = (
     "hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter",
     "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
     "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
-    "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared",
+    "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta",
 )
-KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys")   # HGF_KC_* order
+KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost")   # HGF_KC_* order
 
 _lib = None
 
@@ -65,9 +65,11 @@ def lib():
     L.hgf_prepare_rows.argtypes = [vp, vp, c_int, c_int]
     L.hgf_stats_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
     L.hgf_aggregate_wta_prepared.argtypes = [vp, vp, c_int, c_int, vp, vp, vp, vp]
+    c_float = ctypes.c_float
+    L.hgf_stereo_wta.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, vp, vp, vp, vp]
     for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
                  "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host", "hgf_prepare_rows",
-                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared"):
+                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -192,6 +194,21 @@ class HGF:
                                                _ptr(out.get("labels")), _ptr(out.get("min_cost")),
                                                _ptr(out.get("filtered")), _ptr(out.get("keys"))),
                     "hgf_aggregate_wta_ex")
+        return out
+
+    def stereo_wta(self, left, right, L, label_offset=0, alpha=0.11, tau_color=0.028, tau_grad=0.008, labels=True,
+                   min_cost=False, filtered=False, keys=False, out=None):
+        """hgf_stereo_wta: cost slices of disparities label_offset .. + L - 1 built on the GPU from the two
+        views (S:400 cost), then the HGF aggregation + WTA with the left view as guide."""
+        torch = self._torch
+        self._dev(left, (3, self.H, self.W), torch.float32, "left")
+        self._dev(right, (3, self.H, self.W), torch.float32, "right")
+        out = self._outputs(int(L), labels, min_cost, filtered, keys, out)
+        self._bind_stream()
+        self._check(lib().hgf_stereo_wta(self._h, _ptr(left), _ptr(right), int(L), int(label_offset), float(alpha),
+                                         float(tau_color), float(tau_grad), _ptr(out.get("labels")),
+                                         _ptr(out.get("min_cost")), _ptr(out.get("filtered")), _ptr(out.get("keys"))),
+                    "hgf_stereo_wta")
         return out
 
     def prepare_rows(self, guide, y0, y1):

@@ -27,6 +27,8 @@ struct hgf_ctx {
   int32_t* best_label = nullptr;
   // host-buffer path staging (lazily allocated)
   float* st_guide = nullptr;
+  float* sv_grad = nullptr;    // hgf_stereo_wta: dx of the channel mean of the left / right views [2][H][W]
+  float* sv_cost = nullptr;    // hgf_stereo_wta: one chunk of constructed cost slices [lcap][H][W]
   float* st_vol[2] = {nullptr, nullptr};
   int32_t* st_labels = nullptr;
   int st_chunk = 0;
@@ -115,6 +117,8 @@ void release(hgf_ctx* h) {
   cudaFree(h->best_cost);
   cudaFree(h->best_label);
   cudaFree(h->st_guide);
+  cudaFree(h->sv_grad);
+  cudaFree(h->sv_cost);
   cudaFree(h->st_vol[0]);
   cudaFree(h->st_vol[1]);
   cudaFree(h->st_labels);
@@ -254,9 +258,11 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
   return true;
 }
 
-// Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.
-hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
-                  int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
+// Steps 3-4 over labels [0, L) of vol, chunked by the coefficient buffer capacity.  build_chunk (optional)
+// constructs the chunk's slices [c0, c0 + Lc) and returns their device pointer instead of vol + c0 HW.
+template <class BuildChunk>
+hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
+                       int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out, BuildChunk build_chunk) {
   const long long HW = (long long)h->W * h->H;
   // balanced chunks (e.g. 256 labels with a 147-label capacity -> 2 x 128, not 128 + 128 + ... tails)
   const int nchunks = (L + h->lcap - 1) / h->lcap;
@@ -265,7 +271,10 @@ hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int l
   if (step > h->lcap) step = h->lcap;
   for (int c0 = 0; c0 < L; c0 += step) {
     const int Lc = (L - c0 < step) ? (L - c0) : step;
-    cudaError_t e = launch_coef_chunk(h, guide, vol + (long long)c0 * HW, Lc);
+    const float* chunk = vol ? vol + (long long)c0 * HW : nullptr;
+    cudaError_t e = build_chunk(c0, Lc, &chunk);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cost construction");
+    e = launch_coef_chunk(h, guide, chunk, Lc);
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
     a.G = h->G;
@@ -285,6 +294,12 @@ hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int l
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
   }
   return HGF_OK;
+}
+
+hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
+                  int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
+  return slices_impl(h, guide, vol, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out,
+                     [](int, int, const float**) { return cudaSuccess; });
 }
 
 }  // namespace
@@ -476,6 +491,53 @@ hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, in
   if (s != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
   return slices(h, nullptr, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
+}
+
+hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, int L, int label_offset,
+                          float alpha, float tau_color, float tau_grad, int32_t* labels_out, float* min_cost_out,
+                          float* filtered_out, int64_t* keys_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!left || !right) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null view pointer");
+  if (h->m != 3) return fail(h, HGF_ERR_INVALID_ARGUMENT, "hgf_stereo_wta needs a 3-channel guide (the left view)");
+  if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
+  if (label_offset < 0 || (long long)label_offset + L > 2147483647LL)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
+  if (!(alpha >= 0.0f && alpha <= 1.0f) || !(tau_color >= 0.0f) || !(tau_grad >= 0.0f) || !std::isfinite(tau_color) ||
+      !std::isfinite(tau_grad))
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "cost parameters: 0 <= alpha <= 1, finite non-negative thresholds");
+  if (!labels_out && !min_cost_out && !filtered_out && !keys_out)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
+  const size_t HW = (size_t)h->W * h->H;
+  cudaError_t e;
+  if (!h->sv_grad) {
+    if ((e = cudaMalloc(&h->sv_grad, sizeof(float) * 2 * HW)) != cudaSuccess ||
+        (e = cudaMalloc(&h->sv_cost, sizeof(float) * HW * (size_t)h->lcap)) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(h->sv_grad);
+      h->sv_grad = nullptr;
+      return fail(h, e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA, "cost scratch allocation");
+    }
+  }
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  if ((s = frame_stats(h, left, 0, h->H)) != HGF_OK) return s;
+  e = traced(h, HGF_KC_COST, h->stream, [&] {
+    cudaError_t e2 = hgf::launch_stereo_grad(left, h->sv_grad, h->W, h->H, h->stream);
+    return e2 != cudaSuccess ? e2 : hgf::launch_stereo_grad(right, h->sv_grad + HW, h->W, h->H, h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "stereo gradients");
+  const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
+  return slices_impl(h, left, nullptr, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out,
+                     [&](int c0, int Lc, const float** chunk) {
+                       *chunk = h->sv_cost;
+                       return traced(h, HGF_KC_COST, h->stream, [&] {
+                         return hgf::launch_stereo_cost(left, right, h->sv_grad, h->sv_grad + HW, h->sv_cost, h->W,
+                                                        h->H, label_offset + c0, Lc, alpha, tau_color, tau_grad,
+                                                        h->stream);
+                       });
+                     });
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {

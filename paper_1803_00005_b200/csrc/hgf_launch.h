@@ -59,6 +59,11 @@ bool fast_path_ok(int m, int d, int r);
 cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo,
                              int W, int H, int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st);
+// Stereo cost construction (hgf_stereo.cu): dx of the channel mean of a 3-channel view; cost slices of
+// disparities [d0, d0 + Lc) into cost [Lc][H][W].
+cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cudaStream_t st);
+cudaError_t launch_stereo_cost(const float* left, const float* right, const float* gl, const float* gr, float* cost,
+                               int W, int H, int d0, int Lc, float a, float tc, float tg, cudaStream_t st);
 }  // namespace hgf
 
 namespace hgf {

@@ -240,3 +240,58 @@ def test_prepared_path_unsupported_config_fails_loudly():
     with pytest.raises(HGFError):
         h.stats_view()
     h.close()
+
+
+@pytest.mark.parametrize("W,H,L,label_offset,d,r,mode", [(150, 90, 24, 0, 2, 9, "hgf"), (97, 61, 40, 5, 1, 4, "gf"),
+                                                          (64, 48, 8, 0, 1, 2, "hgf")])
+def test_stereo_wta_parity(W, H, L, label_offset, d, r, mode):
+    """NEXT-2: cost slices built on the GPU from the two views, then aggregation + WTA, against the
+    oracle's own stereo cost filtered by the oracle."""
+    torch = _torch()
+    scene = synth.make_stereo_scene(W, H, L + label_offset, seed=50 + W)
+    h = _hgf(W, H, 3, d, r, 0.05, mode)
+    out = h.stereo_wta(torch.from_numpy(scene.left).cuda(), torch.from_numpy(scene.right).cuda(), L,
+                       label_offset=label_offset, labels=True, min_cost=True, filtered=True, keys=True)
+    torch.cuda.synchronize()
+    C = O.stereo_cost(scene.left, scene.right, L, l0=label_offset)
+    Z = O.hgf_filter(scene.left, C, 0.05, r, d, mode=mode)
+    s_v = float(np.abs(C).max())
+    check_z(out["filtered"].cpu().numpy(), Z, s_v)
+    lab = out["labels"].cpu().numpy()
+    check_labels(lab - label_offset, Z, s_v)
+    h.close()
+
+
+def test_stereo_wta_equals_volume_path():
+    """The constructed slices match the workload generator's volume: same labels (off near-ties) and
+    filtered costs within fp32 rounding of the cost arithmetic."""
+    torch = _torch()
+    W, H, L = 200, 120, 48
+    scene = synth.make_stereo_scene(W, H, L, seed=61)
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    gl = torch.from_numpy(scene.left).cuda()
+    a = h.stereo_wta(gl, torch.from_numpy(scene.right).cuda(), L, labels=True, filtered=True)
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    b = h.aggregate_wta_ex(gl, vol, labels=True, filtered=True)
+    torch.cuda.synchronize()
+    fa, fb = a["filtered"].cpu().numpy(), b["filtered"].cpu().numpy()
+    s_v = float(vol.abs().max())
+    check_z(fa, fb.astype(np.float64), s_v, tol=1e-5)
+    assert np.mean(a["labels"].cpu().numpy() == b["labels"].cpu().numpy()) >= 0.9999
+    h.close()
+
+
+def test_stereo_wta_invalid_arguments():
+    torch = _torch()
+    from paper_1803_00005_b200 import HGFError
+    h = _hgf(32, 16, 1, 2, 2, 0.05, "hgf")                 # n_guide = 1: no stereo views
+    v = torch.zeros(3, 16, 32, device="cuda")
+    with pytest.raises(HGFError):
+        h.stereo_wta(v, v, 4)
+    h.close()
+    h = _hgf(32, 16, 3, 1, 2, 0.05, "hgf")
+    with pytest.raises(HGFError):
+        h.stereo_wta(v, v, 4, alpha=1.5)
+    with pytest.raises(HGFError):
+        h.stereo_wta(v, v, 0)
+    h.close()
