@@ -295,3 +295,23 @@ def test_stereo_wta_invalid_arguments():
     with pytest.raises(HGFError):
         h.stereo_wta(v, v, 0)
     h.close()
+
+
+def test_stereo_rectangle_shift_fixture_on_gpu():
+    """SPEC S:403 fixture through hgf_stereo_wta: disparity 4 recovered inside the shifted rectangle."""
+    torch = _torch()
+    H, W, L, s = 24, 48, 8, 4
+    rng = np.random.default_rng(7)
+    left = np.full((3, H, W), 0.3, dtype=np.float32)
+    tex = (0.5 + 0.3 * rng.random((3, 10, 14))).astype(np.float32)
+    left[:, 7:17, 20:34] = tex
+    right = np.full((3, H, W), 0.3, dtype=np.float32)
+    right[:, 7:17, 20 - s:34 - s] = tex
+    h = _hgf(W, H, 3, 1, 2, 0.05, "hgf")
+    out = h.stereo_wta(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda(), L, filtered=True)
+    torch.cuda.synchronize()
+    lab = out["labels"].cpu().numpy()
+    assert np.all(lab[9:15, 23:31] == s)
+    Z = O.hgf_filter(left, O.stereo_cost(left, right, L), 0.05, 2, 1)
+    check_z(out["filtered"].cpu().numpy(), Z, float(np.abs(O.stereo_cost(left, right, L)).max()))
+    h.close()

@@ -342,3 +342,19 @@ def test_stereo_cost_agrees_with_the_workload_generator():
     ora = O.stereo_cost(scene.left, scene.right, 12)
     # the generator works in float32 on [0, 1] intensities: a few ulps (6e-8) of the gradient terms
     assert np.abs(gen - ora).max() < 3e-7
+
+
+def test_stereo_rectangle_shift_fixture_recovers_disparity():
+    """SPEC S:403 [DERIVED]: uniform background, a textured rectangle shifted by 4 px between the views ->
+    WTA after HGF filtering recovers disparity 4 inside the rectangle (background: disparity 0)."""
+    H, W, L, s = 24, 48, 8, 4
+    rng = np.random.default_rng(7)
+    left = np.full((3, H, W), 0.3)
+    tex = 0.5 + 0.3 * rng.random((3, 10, 14))
+    left[:, 7:17, 20:34] = tex
+    right = np.full((3, H, W), 0.3)
+    right[:, 7:17, 20 - s:34 - s] = tex
+    C = O.stereo_cost(left, right, L)
+    Z = O.hgf_filter(left, C, 0.05, 2, 1)
+    lab = O.wta(Z)
+    assert np.all(lab[9:15, 23:31] == s)
