@@ -36,7 +36,7 @@ __all__ = [
     "poly_guidance", "gram_planes", "alpha_recursion", "weights_eq13",
     "hgf_filter", "hgf_filter_brute", "gf_he",
     "wta", "aggregate_wta", "pack_keys", "unpack_keys",
-    "stereo_cost", "stereo_cost_brute",
+    "stereo_cost", "stereo_cost_brute", "segmentation_cost",
 ]
 
 MODE_HGF = "hgf"
@@ -446,3 +446,35 @@ def stereo_cost_brute(left: np.ndarray, right: np.ndarray, L: int, l0: int = 0, 
                 out[k, y, x] = alpha * min(col, tau_c) + (1 - alpha) * min(grd, tau_g)
     return out
 
+
+
+# ----------------------------------------------------------------------------- segmentation cost
+SEG_BINS = 32
+
+
+def segmentation_cost(image: np.ndarray, fg: np.ndarray, bg: np.ndarray, bins: int = SEG_BINS) -> np.ndarray:
+    """Two cost slices (0 = foreground, 1 = background) for the segmentation workload (labels are
+    foreground / background, costs as in Hosni et al.; the form is SPEC S:406-409): per class, per-channel
+    histograms of the seed pixels' colours with `bins` bins (bin = min(floor(v * bins), bins - 1) of a [0,1]
+    intensity), Laplace-smoothed (+1 per bin): p_c(b) = (count_c(b) + 1) / (N + bins).  The colour
+    likelihood is the product over channels (readings S1, S2 in DESIGN.md), the cost its negative log
+    normalised by its largest possible value m log(N + bins) (a colour no seed has), so each slice lies in
+    (0, 1].
+    image: (m, H, W); fg, bg: boolean (H, W) seed masks, both non-empty.  float64 (2, H, W)."""
+    img = np.asarray(image, dtype=np.float64)
+    m = img.shape[0]
+    b = np.minimum(np.floor(img * bins), bins - 1).astype(np.int64)
+    b = np.maximum(b, 0)
+    out = []
+    for seeds in (fg, bg):
+        seeds = np.asarray(seeds, dtype=bool)
+        N = int(seeds.sum())
+        if N == 0:
+            raise ValueError("empty seed set")
+        nll = np.zeros(img.shape[1:])
+        for c in range(m):
+            counts = np.bincount(b[c][seeds], minlength=bins).astype(np.float64)
+            p = (counts + 1.0) / (N + bins)
+            nll -= np.log(p[b[c]])
+        out.append(nll / (m * np.log(N + bins)))
+    return np.stack(out)

@@ -358,3 +358,41 @@ def test_stereo_rectangle_shift_fixture_recovers_disparity():
     Z = O.hgf_filter(left, C, 0.05, 2, 1)
     lab = O.wta(Z)
     assert np.all(lab[9:15, 23:31] == s)
+
+
+# ----------------------------------------------------------------------------- segmentation cost (NEXT-4)
+def _two_colour_scene():
+    H, W = 20, 30
+    img = np.empty((3, H, W))
+    img[:] = np.array([0.9, 0.2, 0.1])[:, None, None]          # foreground colour
+    img[:, :, 15:] = np.array([0.1, 0.3, 0.8])[:, None, None]  # background colour (right half)
+    fg = np.zeros((H, W), bool)
+    bg = np.zeros((H, W), bool)
+    fg[10, 5] = True
+    bg[10, 25] = True
+    return img, fg, bg
+
+
+def test_segmentation_cost_spec_examples():
+    img, fg, bg = _two_colour_scene()
+    C = O.segmentation_cost(img, fg, bg)
+    assert C.shape == (2, 20, 30) and C.min() > 0.0 and C.max() <= 1.0          # 1 = colour never seeded
+    # a colour seen only in the fg seeds costs less as fg (S:408 example 1)
+    assert np.all(C[0][:, :15] < C[1][:, :15]) and np.all(C[1][:, 15:] < C[0][:, 15:])
+    # identical seed distributions -> identical slices (S:408 example 2)
+    same = O.segmentation_cost(img, fg, fg)
+    assert np.abs(same[0] - same[1]).max() <= 1e-12
+    # closed form for one seed pixel: p = 2/33 in its bin, 1/33 elsewhere (Laplace +1, 32 bins)
+    assert np.isclose(C[0][10, 5], -3 * np.log(2 / 33) / (3 * np.log(33)), rtol=0, atol=1e-15)
+    assert np.isclose(C[1][10, 5], -3 * np.log(1 / 33) / (3 * np.log(33)), rtol=0, atol=1e-15)
+    with pytest.raises(ValueError):
+        O.segmentation_cost(img, fg, np.zeros_like(bg))
+
+
+def test_segmentation_two_colour_fixture_labels_regions():
+    """S:409 [DERIVED]: two-colour image, one seed pixel per region -> WTA after HGF filtering labels each
+    region (0 = fg left, 1 = bg right) away from the boundary."""
+    img, fg, bg = _two_colour_scene()
+    C = O.segmentation_cost(img, fg, bg)
+    lab = O.wta(O.hgf_filter(img, C, 0.05, 2, 1))
+    assert np.all(lab[:, :12] == 0) and np.all(lab[:, 18:] == 1)
