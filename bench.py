@@ -224,6 +224,37 @@ def stereo_leg(h, scene, L, W, H, args, torch):
             "api": "hgf_stereo_wta (SURVEY 8(f) NEXT-2: S:400 cost slices built per chunk on the GPU)"}
 
 
+def segment_leg(args, torch):
+    """NEXT-4 (hgf_segment): foreground/background labels of a 1920x1080 frame (L = 2, seed-histogram costs
+    built on the GPU), the paper's segmentation workload; device ms per frame."""
+    import synth
+    from paper_1803_00005_b200 import HGF
+    W, H = 1920, 1080
+    scene = synth.make_stereo_scene(W, H, 8, 3)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    img = torch.from_numpy(scene.left).to(dev)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    fg = (torch.rand((H, W), generator=g) < 0.01).to(torch.uint8)
+    fg[:, W // 2:] = 0
+    bg = (torch.rand((H, W), generator=g) < 0.01).to(torch.uint8)
+    bg[:, :W // 2] = 0
+    fg, bg = fg.to(dev), bg.to(dev)
+    h = HGF(W, H, 3, 2, 9, 0.05)
+    lab = torch.empty((H, W), dtype=torch.int32, device=dev)
+    for _ in range(max(1, args.warmup)):
+        h.segment(img, fg, bg, out={"labels": lab})
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        h.segment(img, fg, bg, out={"labels": lab})
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / args.steps * 1e3
+    h.close()
+    return {"ms_per_frame": ms, "workload": "1920x1080, RGB degree-2 guidance (n=6), r=9, L=2 (fg/bg), 1% seeds",
+            "timing": "wall clock around synchronised calls (hgf_segment reads the seed counts back once)",
+            "api": "hgf_segment (SURVEY 8(f) NEXT-4)"}
+
+
 # ----------------------------------------------------------------------------- own arm
 def main():
     args = parse()
@@ -356,6 +387,7 @@ def main():
     # e2e through the public API with host buffers
     e2e = None
     stereo = None
+    segmentation = None
     if not args.no_e2e:
         if world == 1:
             vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
@@ -373,6 +405,7 @@ def main():
                    "api": "hgf_aggregate_wta_host (chunked H2D overlapped with compute)"}
             del vol_h
             stereo = stereo_leg(h, scene, L, W, H, args, torch)
+            segmentation = segment_leg(args, torch)
         else:
             vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
             vol_h.copy_(vol)
@@ -414,6 +447,7 @@ def main():
                 "hbm": {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
                         "alg_bytes_per_step": alg_bytes(W, H, L, m)},
                 "stage_ms_per_step": stage_ms, "cpu_baseline": cpu, "e2e": e2e, "stereo_cost_on_gpu": stereo,
+                "segmentation": segmentation,
                 "gpu_launches": int(lt.item()), "clocks": clk}
         print(json.dumps(line), flush=True)
     h.close()

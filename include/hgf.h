@@ -127,6 +127,17 @@ HGF_API hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* 
                                   float alpha, float tau_color, float tau_grad, int32_t* labels_out,
                                   float* min_cost_out, float* filtered_out, int64_t* keys_out);
 
+/* Foreground / background segmentation (cost form of SPEC S:406-409):
+ * two cost slices (label 0 = foreground, 1 = background) from per-class, per-channel 32-bin histograms of
+ * the seed pixels' colours, Laplace-smoothed: p_c(b) = (count_c(b) + 1) / (N_c + 32), cost
+ * C_c(x) = -sum_ch log p_c(bin(I_ch(x))) / (m log(N_c + 32)) in (0, 1], bin(v) = min(floor(32 v), 31);
+ * then steps 1-4 with the image as the guide (L = 2).  image: device [n_guide][H][W] f32 in [0,1];
+ * fg_seeds, bg_seeds: device [H][W] u8 masks (non-zero = seed).  Outputs as hgf_aggregate_wta_ex
+ * (labels are 0 / 1; at least one non-null).  HGF_ERR_INVALID_ARGUMENT for an empty seed set (checked
+ * with one small device-to-host read, which synchronises the handle's stream). */
+HGF_API hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds, const uint8_t* bg_seeds,
+                               int32_t* labels_out, float* min_cost_out, float* filtered_out);
+
 /* Row-sharded frame preparation.  Steps 1-2 of the path for a row band:
  * the polynomial guidance for the whole frame (cheap, needed by every slice kernel) and the
  * label-independent statistics (Prop 1 recursion, Eq4 P:143-151 with readings F1/F2) of image rows

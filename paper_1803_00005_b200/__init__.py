@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = (
     "hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter",
     "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
     "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
-    "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta",
+    "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment",
 )
 KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost")   # HGF_KC_* order
 
@@ -67,9 +67,10 @@ def lib():
     L.hgf_aggregate_wta_prepared.argtypes = [vp, vp, c_int, c_int, vp, vp, vp, vp]
     c_float = ctypes.c_float
     L.hgf_stereo_wta.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, vp, vp, vp, vp]
+    L.hgf_segment.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
                  "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host", "hgf_prepare_rows",
-                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta"):
+                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -209,6 +210,20 @@ class HGF:
                                          float(tau_color), float(tau_grad), _ptr(out.get("labels")),
                                          _ptr(out.get("min_cost")), _ptr(out.get("filtered")), _ptr(out.get("keys"))),
                     "hgf_stereo_wta")
+        return out
+
+    def segment(self, image, fg_seeds, bg_seeds, labels=True, min_cost=False, filtered=False, out=None):
+        """hgf_segment: foreground (0) / background (1) labels from seed masks (uint8 or bool CUDA tensors)."""
+        torch = self._torch
+        self._dev(image, (self.m, self.H, self.W), torch.float32, "image")
+        fg = fg_seeds.to(torch.uint8).contiguous() if fg_seeds.dtype != torch.uint8 else fg_seeds
+        bg = bg_seeds.to(torch.uint8).contiguous() if bg_seeds.dtype != torch.uint8 else bg_seeds
+        self._dev(fg, (self.H, self.W), torch.uint8, "fg_seeds")
+        self._dev(bg, (self.H, self.W), torch.uint8, "bg_seeds")
+        out = self._outputs(2, labels, min_cost, filtered, False, out)
+        self._bind_stream()
+        self._check(lib().hgf_segment(self._h, _ptr(image), _ptr(fg), _ptr(bg), _ptr(out.get("labels")),
+                                      _ptr(out.get("min_cost")), _ptr(out.get("filtered"))), "hgf_segment")
         return out
 
     def prepare_rows(self, guide, y0, y1):

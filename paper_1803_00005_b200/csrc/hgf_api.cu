@@ -29,6 +29,8 @@ struct hgf_ctx {
   float* st_guide = nullptr;
   float* sv_grad = nullptr;    // hgf_stereo_wta: dx of the channel mean of the left / right views [2][H][W]
   float* sv_cost = nullptr;    // hgf_stereo_wta: one chunk of constructed cost slices [lcap][H][W]
+  float* sg_cost = nullptr;    // hgf_segment: the two cost slices [2][H][W]
+  int* sg_counts = nullptr;    // hgf_segment: seed histograms [2][m][32] then seed counts [2]
   float* st_vol[2] = {nullptr, nullptr};
   int32_t* st_labels = nullptr;
   int st_chunk = 0;
@@ -119,6 +121,8 @@ void release(hgf_ctx* h) {
   cudaFree(h->st_guide);
   cudaFree(h->sv_grad);
   cudaFree(h->sv_cost);
+  cudaFree(h->sg_cost);
+  cudaFree(h->sg_counts);
   cudaFree(h->st_vol[0]);
   cudaFree(h->st_vol[1]);
   cudaFree(h->st_labels);
@@ -538,6 +542,50 @@ hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, i
                                                         h->stream);
                        });
                      });
+}
+
+hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds, const uint8_t* bg_seeds,
+                       int32_t* labels_out, float* min_cost_out, float* filtered_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!image || !fg_seeds || !bg_seeds) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!labels_out && !min_cost_out && !filtered_out) return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
+  const size_t HW = (size_t)h->W * h->H;
+  const int nbins = 2 * h->m * 32;
+  cudaError_t e;
+  if (!h->sg_cost) {
+    if ((e = cudaMalloc(&h->sg_cost, sizeof(float) * 2 * HW)) != cudaSuccess ||
+        (e = cudaMalloc(&h->sg_counts, sizeof(int) * (nbins + 2))) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(h->sg_cost);
+      h->sg_cost = nullptr;
+      return fail(h, e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA, "segmentation scratch");
+    }
+  }
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  int* seeds = h->sg_counts + nbins;
+  e = traced(h, HGF_KC_COST, h->stream, [&] {
+    cudaError_t e2 = cudaMemsetAsync(h->sg_counts, 0, sizeof(int) * (nbins + 2), h->stream);
+    return e2 != cudaSuccess ? e2
+                             : hgf::launch_seg_hist(image, fg_seeds, bg_seeds, h->m, h->W, h->H, h->sg_counts, seeds,
+                                                    h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "seed histograms");
+  // empty seed sets are an argument error: the one host read of this entry point
+  int nseeds[2] = {0, 0};
+  if ((e = cudaMemcpyAsync(nseeds, seeds, sizeof(nseeds), cudaMemcpyDeviceToHost, h->stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(h->stream)) != cudaSuccess)
+    return cuda_fail(h, e, "seed count read");
+  if (nseeds[0] == 0 || nseeds[1] == 0) return fail(h, HGF_ERR_INVALID_ARGUMENT, "empty foreground or background seed set");
+  e = traced(h, HGF_KC_COST, h->stream, [&] {
+    return hgf::launch_seg_cost(image, h->sg_counts, seeds, h->m, h->W, h->H, h->sg_cost, h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "segmentation cost");
+  if ((s = frame_stats(h, image, 0, h->H)) != HGF_OK) return s;
+  const int do_wta = (labels_out || min_cost_out) ? 1 : 0;
+  return slices(h, image, h->sg_cost, 2, 0, filtered_out, do_wta, labels_out, min_cost_out, nullptr);
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {

@@ -64,6 +64,12 @@ cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st);
 cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cudaStream_t st);
 cudaError_t launch_stereo_cost(const float* left, const float* right, const float* gl, const float* gr, float* cost,
                                int W, int H, int d0, int Lc, float a, float tc, float tg, cudaStream_t st);
+// Segmentation costs (hgf_stereo.cu): seed histograms counts [2][m][32], seeds [2] (zeroed by the caller),
+// then the two cost slices [2][H][W].
+cudaError_t launch_seg_hist(const float* img, const uint8_t* fg, const uint8_t* bg, int m, int W, int H, int* counts,
+                            int* seeds, cudaStream_t st);
+cudaError_t launch_seg_cost(const float* img, const int* counts, const int* seeds, int m, int W, int H, float* cost,
+                            cudaStream_t st);
 }  // namespace hgf
 
 namespace hgf {

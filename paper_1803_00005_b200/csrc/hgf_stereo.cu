@@ -101,3 +101,81 @@ cudaError_t launch_stereo_cost(const float* left, const float* right, const floa
 }
 
 }  // namespace hgf
+
+// ----------------------------------------------------------------------------- segmentation (NEXT-4)
+// Cost of the two labels (0 = foreground, 1 = background) from per-class per-channel colour histograms of
+// the seed pixels (P:648-649 defers to Hosni et al.; form of SPEC S:406-409, readings S1/S2 in DESIGN.md):
+//   bin(v) = min(floor(32 v), 31), p_c(b) = (count_c(b) + 1) / (N_c + 32),
+//   C_c(x) = -sum_ch log p_c(bin(I_ch(x))) / (m log(N_c + 32))   in (0, 1].
+namespace hgf {
+namespace {
+
+constexpr int SEG_BINS = 32;
+
+__device__ __forceinline__ int seg_bin(float v) {
+  const float f = floorf(v * (float)SEG_BINS);
+  return f < 0.0f ? 0 : (f > (float)(SEG_BINS - 1) ? SEG_BINS - 1 : (int)f);
+}
+
+// counts: [2][m][32] int, seeds: [2] int (zeroed by the caller)
+__global__ void k_seg_hist(const float* __restrict__ img, const uint8_t* __restrict__ fg,
+                           const uint8_t* __restrict__ bg, int m, int W, int H, int* __restrict__ counts,
+                           int* __restrict__ seeds) {
+  extern __shared__ int sh[];                      // [2][m][32] + [2]
+  const int nb = 2 * m * SEG_BINS;
+  for (int i = threadIdx.x; i < nb + 2; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const long long HW = (long long)W * H;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
+    const bool f = fg[p] != 0, b = bg[p] != 0;
+    if (!f && !b) continue;
+    for (int c = 0; c < m; ++c) {
+      const int bin = seg_bin(img[c * HW + p]);
+      if (f) atomicAdd(&sh[(0 * m + c) * SEG_BINS + bin], 1);
+      if (b) atomicAdd(&sh[(1 * m + c) * SEG_BINS + bin], 1);
+    }
+    if (f) atomicAdd(&sh[nb], 1);
+    if (b) atomicAdd(&sh[nb + 1], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (sh[i]) atomicAdd(&counts[i], sh[i]);
+  if (threadIdx.x < 2 && sh[nb + threadIdx.x]) atomicAdd(&seeds[threadIdx.x], sh[nb + threadIdx.x]);
+}
+
+__global__ void k_seg_cost(const float* __restrict__ img, const int* __restrict__ counts,
+                           const int* __restrict__ seeds, int m, int W, int H, float* __restrict__ cost) {
+  const long long HW = (long long)W * H;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
+    for (int k = 0; k < 2; ++k) {
+      const float den = (float)seeds[k] + (float)SEG_BINS;
+      float nll = 0.0f;
+      for (int c = 0; c < m; ++c) {
+        const int bin = seg_bin(img[c * HW + p]);
+        nll -= logf(((float)counts[(k * m + c) * SEG_BINS + bin] + 1.0f) / den);
+      }
+      cost[k * HW + p] = nll / ((float)m * logf(den));
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_seg_hist(const float* img, const uint8_t* fg, const uint8_t* bg, int m, int W, int H, int* counts,
+                            int* seeds, cudaStream_t st) {
+  const long long HW = (long long)W * H;
+  const int blocks = (int)((HW + 255) / 256 < 148 * 4 ? (HW + 255) / 256 : 148 * 4);
+  const size_t smem = sizeof(int) * (2 * (size_t)m * SEG_BINS + 2);
+  k_seg_hist<<<blocks, 256, smem, st>>>(img, fg, bg, m, W, H, counts, seeds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seg_cost(const float* img, const int* counts, const int* seeds, int m, int W, int H, float* cost,
+                            cudaStream_t st) {
+  const long long HW = (long long)W * H;
+  const int blocks = (int)((HW + 255) / 256 < 148 * 16 ? (HW + 255) / 256 : 148 * 16);
+  k_seg_cost<<<blocks, 256, 0, st>>>(img, counts, seeds, m, W, H, cost);
+  return cudaGetLastError();
+}
+
+}  // namespace hgf
