@@ -59,7 +59,7 @@ constexpr int MMAW = NVW;                    // warp that allocates TMEM and iss
 constexpr int NEW = 4;                       // epilogue warps (one per TMEM lane quadrant)
 constexpr int EW0 = NVW + 1;                 // first epilogue warp
 constexpr int THREADS = (NVW + 1 + NEW) * 32;   // 480
-constexpr int BAR_B = 2;                     // named barrier: V warps arrive (B written), MMA warp syncs
+
 constexpr int BAR_V = 1;                     // named barrier among the V warps
 constexpr int SPX = kStatsAos;               // floats per statistics record
 static_assert(KCMAX <= BXP && TX + 2 * RMAX + 3 <= BXP && TX + 2 * RMAX <= CXP, "strip geometry");
@@ -73,7 +73,7 @@ struct Geom4 {
   static constexpr int PROW = LB * BXP;                          // floats: one cost row of the 16 labels
   static constexpr int GROW = ((NC > 0 ? NC : 1) * BXP + 31) / 32 * 32;
   static constexpr int STAGE = 2 * PROW + 2 * GROW;              // floats per TMA stage
-  static constexpr size_t SMEM = 2 * (size_t)BPLANE + 2 * (size_t)STAGE * 4 + 64;
+  static constexpr size_t SMEM = 2 * (size_t)BPLANE + 2 * (size_t)STAGE * 4 + 8 * sizeof(uint64_t);
   static_assert(N % 16 == 0 && N <= 128, "MMA N / TMEM double buffer");
   static_assert(LB == 16 && K <= 7, "epilogue: 4-label batches of <= 32 columns");
   static_assert(NS + 1 <= SPX, "statistics record");
@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tma_full = bar;          // [2] stage landed
   uint64_t* mma_done = bar + 2;      // [2] MMAs of the row in D[b] completed (B free again)
   uint64_t* d_free = bar + 4;        // [2] epilogue warps finished reading D[b]
+  uint64_t* b_full = bar + 6;        // [2] every V warp wrote row i's B (row parity i & 1)
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int x0 = blockIdx.x * TX;
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       cuda::ptx::mbarrier_init(&tma_full[i], 1);
       cuda::ptx::mbarrier_init(&mma_done[i], 1);
       cuda::ptx::mbarrier_init(&d_free[i], NEW);
+      cuda::ptx::mbarrier_init(&b_full[i], NVW);
     }
     cuda::ptx::fence_mbarrier_init(cuda::ptx::sem_release, cuda::ptx::scope_cluster);
   }
@@ -230,7 +232,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
       }
       tc::fence_proxy_async_smem();
-      asm volatile("bar.arrive %0, %1;" ::"r"(BAR_B), "r"(NV + 32) : "memory");   // B of row i written
+      __syncwarp();
+      if (lane == 0) cuda::ptx::mbarrier_arrive(&b_full[i & 1]);   // this warp's part of row i's B is written
     }
   } else if (warp == MMAW) {
     // ============================ MMA warp ============================
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ksteps = KC / 8;
     for (int y = Y0; y < Y1; ++y) {
       const int i = y - Y0, b = i & 1;
-      nsync(BAR_B, NV + 32);
+      mbar_wait_parity(&b_full[b], (i >> 1) & 1);
       if (lane == 0) {
         if (i >= 2) mbar_wait_parity(&d_free[b], ((i - 2) >> 1) & 1);
         tc::fence_after();
