@@ -31,6 +31,7 @@ struct hgf_ctx {
   float* sv_cost = nullptr;    // hgf_stereo_wta: one chunk of constructed cost slices [lcap][H][W]
   float* sg_cost = nullptr;    // hgf_segment: the two cost slices [2][H][W]
   int* sg_counts = nullptr;    // hgf_segment: seed histograms [2][m][32] then seed counts [2]
+  double* st3_scratch = nullptr;   // k_stats3 (n >= kStats3MinN): Gram planes + one batch of row sums
   float* st_vol[2] = {nullptr, nullptr};
   int32_t* st_labels = nullptr;
   int st_chunk = 0;
@@ -123,6 +124,7 @@ void release(hgf_ctx* h) {
   cudaFree(h->sv_cost);
   cudaFree(h->sg_cost);
   cudaFree(h->sg_counts);
+  cudaFree(h->st3_scratch);
   cudaFree(h->st_vol[0]);
   cudaFree(h->st_vol[1]);
   cudaFree(h->st_labels);
@@ -153,7 +155,7 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide, int y0, int y1) {
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
     const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
     return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode,
-                             (h->v3coef || h->v4coef) ? 1 : 0, lam0, y0, y1, h->stream);
+                             (h->v3coef || h->v4coef) ? 1 : 0, lam0, y0, y1, h->st3_scratch, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
   return HGF_OK;
@@ -395,6 +397,13 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     release(h);
     delete h;
     return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
+  }
+  if (h->n >= 7) {
+    // optional: without it the statistics fall back to k_stats2 / k_stats (register-spilling at large n)
+    if (cudaMalloc(&h->st3_scratch, sizeof(double) * hgf::stats3_scratch_planes(h->n) * HW) != cudaSuccess) {
+      cudaGetLastError();
+      h->st3_scratch = nullptr;
+    }
   }
   if (h->v3agg && !((long long)h->lcap * K <= (1LL << 31) && make_wbuf_tensor_map(h))) {
     // no TMA descriptor: v2 coefficients + aggregation on the flat layout (fits the allocation)

@@ -54,12 +54,19 @@ cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, 
   }
 
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
-                         float lam0f, int y0, int y1, cudaStream_t st) {
-  // sliding-sum version when all n+1 channel tiles fit in shared memory, else the pairwise v1 kernel
+                         float lam0f, int y0, int y1, double* scratch3, cudaStream_t st) {
   const int TS = 16 + 2 * r;
   // = st2::smem_bytes(n, r): odd-pitch channel tiles, 17-double rows of horizontal sums, vertical sums
   const size_t smem2 = ((size_t)(n + 1) * TS * (TS | 1) * 4 + 15) / 16 * 16 + (size_t)8 * TS * 17 * 8 +
                        (size_t)8 * 16 * 16 * 8 + 16;
+  // k_stats3 (Gram planes + warp-per-pixel recursion) where k_stats2 would spill heavily (n >= kStats3MinN)
+  // or not fit its channel tiles in shared memory (the O(r) v1 kernel) -- measured on the C5 sweep
+  if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= kStats3MinN || (n >= 7 && smem2 > 200 * 1024))) {
+#define CALL(N) st3::stats3_impl<N>(G, stats, scratch3, W, H, r, lam, mode, st)
+    HGF_DISPATCH(n, CALL)
+#undef CALL
+  }
+  // sliding-sum version when all n+1 channel tiles fit in shared memory, else the pairwise v1 kernel
   if (smem2 <= 200 * 1024) {
 #define CALL(N) st2::stats2_impl<N>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st)
     HGF_DISPATCH(n, CALL)

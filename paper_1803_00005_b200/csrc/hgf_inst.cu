@@ -1,6 +1,7 @@
 // Explicit instantiation of the per-channel-count kernels for n = HGF_N (set by the Makefile).
 #include "hgf_kernels.cuh"
 #include "hgf_slice_v2.cuh"
+#include "hgf_stats_v3.cuh"
 
 #ifndef HGF_N
 #error "compile with -DHGF_N=<n>"
@@ -11,6 +12,9 @@ template cudaError_t stats_impl<HGF_N>(const float*, float*, int, int, int, doub
 template cudaError_t coef_impl<HGF_N>(const float*, const float*, const float*, float*, int, int, int, int, float,
                                       cudaStream_t);
 template cudaError_t agg_impl<HGF_N>(const AggArgs&, cudaStream_t);
+namespace st3 {
+template cudaError_t stats3_impl<HGF_N>(const float*, float*, double*, int, int, int, double, int, cudaStream_t);
+}  // namespace st3
 #if HGF_N <= 9
 namespace v2 {
 template cudaError_t agg2_impl<HGF_N>(const AggArgs&, cudaStream_t);

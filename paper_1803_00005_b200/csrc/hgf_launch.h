@@ -26,8 +26,11 @@ cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, 
 // aos = 1: per-pixel records of kStatsAos floats (statistics, then kappa = 1/(lam0f + N)) for k_coef3;
 // needs the k_stats2 path (else cudaErrorInvalidValue).
 // Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).
+// scratch3: (stats3_scratch_planes(n)) * H * W doubles, or null (k_stats3 is used for n >= kStats3MinN).
+constexpr int kStats3MinN = 18;     // always k_stats3 from here; below only when k_stats2 does not fit
+inline long long stats3_scratch_planes(int n) { return (long long)(n + 1) * (n + 2) / 2 - 1 + 32; }
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
-                         float lam0f, int y0, int y1, cudaStream_t st);
+                         float lam0f, int y0, int y1, double* scratch3, cudaStream_t st);
 cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H,
                         int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st);
@@ -107,6 +110,11 @@ cudaError_t launch_coef_v4(int n, const void* tm_vol, const void* tm_g, const fl
 }  // namespace hgf
 
 namespace hgf {
+namespace st3 {
+template <int NC>
+cudaError_t stats3_impl(const float* G, float* stats, double* scratch, int W, int H, int r, double lam, int mode,
+                        cudaStream_t st);
+}  // namespace st3
 namespace st2 {
 template <int NC>
 cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,

@@ -1,0 +1,200 @@
+// Label-independent statistics for many channels, version 3 (n >= 7; BASELINE config 5 sweeps n up to 20).
+//
+// Same quantities as k_stats / k_stats2 (Gram G_ij = B(G_i G_j) in float64, Prop 2; the Prop-1
+// recursion P:134-153 with readings F1/F2; P' = -lambda alpha_{1..n,1..n}, nu_k = B(G_k)/(lambda_0 + N)),
+// organised so that nothing per pixel has to live in one thread's registers: at n = 20 the Gram has 230
+// entries and alpha 441, which k_stats2 spilled to local memory (20-70 ms per 1080p frame).
+//
+//   k_gram_h3  : horizontal window sums of every product plane G_i G_j (i <= j, (0,0) excluded) in float64,
+//                one thread per output pixel, the row segment staged in SMEM -> hs[p][y][x]
+//   k_gram_v3  : vertical sliding sums of hs -> the box-summed Gram planes gram[p][y][x] (float64)
+//   k_recur3   : a CTA takes 32 consecutive pixels: their Gram entries are staged in SMEM with coalesced
+//                loads (lane = pixel), then one warp per pixel runs the recursion with lane i holding row i
+//                of alpha in registers (u_i: a dot product per lane; the quadratic form: a warp reduction;
+//                the rank-one update: per lane, with u broadcast from SMEM); the outputs are staged in SMEM
+//                and written plane by plane (lane = pixel).
+#pragma once
+#include "hgf_common.cuh"
+#include "hgf_launch.h"
+
+namespace hgf {
+namespace st3 {
+
+constexpr int HX = 128;          // k_gram_h3 / k_gram_v3: pixels per CTA along x
+constexpr int VROWS = 32;        // k_gram_v3: output rows per CTA (vertical sliding restarts per CTA)
+constexpr int PIX = 32;          // k_recur3: pixels per CTA
+constexpr int RW = 8;            // k_recur3: warps per CTA
+constexpr int PB = 32;           // product planes per horizontal/vertical batch (bounds the scratch)
+
+__host__ __device__ constexpr int npairs(int NC) { return (NC + 1) * (NC + 2) / 2 - 1; }
+
+// pair index p of (i, j), 0 <= i <= j <= n, (0,0) excluded: row-major over the upper triangle
+__device__ __forceinline__ int pair_index(int i, int j, int K) { return i * K - i * (i - 1) / 2 + (j - i) - 1; }
+
+// One CTA per (row, 128-pixel segment): all K channel rows staged once, then every pair of the batch.
+template <int NC>
+__global__ void __launch_bounds__(HX) k_gram_h3(const float* __restrict__ G, double* __restrict__ hs, int W, int H,
+                                                 int r, int p0, int pb) {
+  constexpr int K = NC + 1;
+  extern __shared__ float row[];                    // [K][HX + 2r]: the channel rows (channel 0 = ones)
+  const int y = blockIdx.y, x0 = blockIdx.x * HX, x = x0 + threadIdx.x;
+  const int span = HX + 2 * r;
+  const long long HW = (long long)H * W;
+  for (int e = threadIdx.x; e < K * span; e += HX) {
+    const int c = e / span, xx = x0 - r + (e % span);
+    const bool in = xx >= 0 && xx < W;
+    row[e] = in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)y * W + xx)) : 0.0f;
+  }
+  __syncthreads();
+  if (x >= W) return;
+  int i = 0, q = p0 + 1;
+  while (q >= K - i) { q -= K - i; ++i; }
+  int j = i + q;
+  for (int z = 0; z < pb; ++z) {
+    const float* ri = row + i * span + threadIdx.x;
+    const float* rj = row + j * span + threadIdx.x;
+    double acc = 0.0;
+    for (int dx = 0; dx <= 2 * r; ++dx) acc += (double)ri[dx] * (double)rj[dx];
+    hs[(long long)z * HW + (long long)y * W + x] = acc;
+    if (++j == K) { ++i; j = i; }
+  }
+}
+
+template <int NC>   // (templated only so that every per-n translation unit owns its instance)
+__global__ void __launch_bounds__(HX) k_gram_v3(const double* __restrict__ hs, double* __restrict__ gram, int W,
+                                                 int H, int r, int p0) {
+  const int x = blockIdx.x * HX + threadIdx.x, y0 = blockIdx.y * VROWS;
+  if (x >= W) return;
+  const long long HW = (long long)H * W;
+  const double* col = hs + (long long)blockIdx.z * HW + x;
+  double* out = gram + (long long)(p0 + blockIdx.z) * HW + x;
+  const int y1 = min(H, y0 + VROWS);
+  double acc = 0.0;
+  for (int yy = max(0, y0 - r); yy <= min(H - 1, y0 + r); ++yy) acc += col[(long long)yy * W];
+  out[(long long)y0 * W] = acc;
+  for (int y = y0 + 1; y < y1; ++y) {
+    if (y + r < H) acc += col[(long long)(y + r) * W];
+    if (y - r - 1 >= 0) acc -= col[(long long)(y - r - 1) * W];
+    out[(long long)y * W] = acc;
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ gram, float* __restrict__ stats, int W,
+                                                    int H, int r, double lam, int mode) {
+  constexpr int K = NC + 1, NPAIR = npairs(NC), NP = NC * (NC + 1) / 2, NS = NP + NC;
+  static_assert(K <= 32, "one lane per row of alpha");
+  extern __shared__ __align__(16) double sm3[];
+  double* g = sm3;                                  // [NPAIR][PIX]: Gram entries of the CTA's pixels
+  double* ubuf = g + NPAIR * PIX;                   // [RW][32]: u of each warp's current step
+  float* outs = reinterpret_cast<float*>(ubuf + RW * 32);   // [NS][PIX]: staged outputs
+  const long long HW = (long long)H * W;
+  const long long pix0 = (long long)blockIdx.x * PIX;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < NPAIR * PIX; e += RW * 32) {
+    const int p = e / PIX, k = e % PIX;
+    const long long pix = pix0 + k;
+    g[e] = pix < HW ? gram[(long long)p * HW + pix] : 0.0;
+  }
+  __syncthreads();
+  const double inv_lam = 1.0 / lam;
+  const int c0 = (mode == 0) ? 0 : 1;
+  double* u_s = ubuf + warp * 32;
+  for (int k = warp; k < PIX; k += RW) {
+    const long long pix = pix0 + k;
+    if (pix >= HW) break;
+    const int y = (int)(pix / W), x = (int)(pix % W);
+    const double N = (double)window_count(y, x, H, W, r);
+    // Gram entry (a, b) of this pixel (centred over channels 1..n in GF mode, §5.1)
+    auto gm = [&](int a, int b) -> double {
+      const int lo = a < b ? a : b, hi = a < b ? b : a;
+      double v = (lo == 0 && hi == 0) ? N : g[pair_index(lo, hi, K) * PIX + k];
+      if (mode != 0 && lo > 0) v -= g[pair_index(0, lo, K) * PIX + k] * g[pair_index(0, hi, K) * PIX + k] / N;
+      return v;
+    };
+    // lane i holds row i of alpha (a[j] = alpha_ij), rows / columns c0 .. kappa filled so far
+    double a[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) a[j] = 0.0;
+    // F1 (compile-time indices keep a[] in registers)
+    if (c0 == 0) {
+      if (lane == 0) a[0] = -inv_lam / (lam + gm(0, 0));
+    } else if (lane == 1) {
+      a[1] = -inv_lam / (lam + gm(1, 1));
+    }
+#pragma unroll
+    for (int kap = 1; kap < K; ++kap) {
+      if (kap <= c0) continue;
+      // u_i = sum_{m < kap} alpha_im G_m,kap  (lanes c0 .. kap-1)
+      double u = 0.0;
+      if (lane >= c0 && lane < kap) {
+#pragma unroll
+        for (int m = 0; m < kap; ++m)
+          if (m >= c0) u = fma(a[m], gm(m, kap), u);
+      }
+      // quad = sum_i G_kap,i u_i  (warp reduction)
+      double qv = (lane >= c0 && lane < kap) ? gm(kap, lane) * u : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) qv += __shfl_xor_sync(0xffffffffu, qv, off);
+      const double gam = -1.0 / (1.0 + inv_lam * gm(kap, kap) + qv);               // gamma^kappa
+      u_s[lane] = u;
+      __syncwarp();
+      if (lane >= c0 && lane < kap) {
+#pragma unroll
+        for (int j = 0; j < kap; ++j)
+          if (j >= c0) a[j] = fma(gam * u, u_s[j], a[j]);                            // gamma F + alpha (F2)
+        a[kap] = inv_lam * gam * u;
+      } else if (lane == kap) {
+#pragma unroll
+        for (int j = 0; j < kap; ++j)
+          if (j >= c0) a[j] = inv_lam * gam * u_s[j];
+        a[kap] = inv_lam * inv_lam * gam;
+      }
+      __syncwarp();
+    }
+    // outputs: P' = -lambda alpha_{1..n,1..n} (upper triangle, row-major), then nu_k = G_0k / den
+    if (lane >= 1 && lane < K) {
+      const int ai = lane;
+      int s = (ai - 1) * NC - (ai - 1) * (ai - 2) / 2;     // first upper-triangle slot of row ai
+#pragma unroll
+      for (int b = 1; b < K; ++b)
+        if (b >= ai) outs[(s + (b - ai)) * PIX + k] = (float)(-lam * a[b]);
+      const double den = (mode == 0) ? (lam + N) : N;
+      outs[(NP + ai - 1) * PIX + k] = (float)(g[pair_index(0, ai, K) * PIX + k] / den);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < NS * PIX; e += RW * 32) {
+    const int s = e / PIX, k = e % PIX;
+    const long long pix = pix0 + k;
+    if (pix < HW) stats[(long long)s * HW + pix] = outs[e];
+  }
+}
+
+// scratch: (npairs(NC) + PB) * H * W doubles (the Gram planes, then one batch of horizontal sums)
+template <int NC>
+cudaError_t stats3_impl(const float* G, float* stats, double* scratch, int W, int H, int r, double lam, int mode,
+                        cudaStream_t st) {
+  constexpr int NPAIR = npairs(NC), NS = NC * (NC + 1) / 2 + NC;
+  const long long HW = (long long)H * W;
+  double* gram = scratch;
+  double* hs = scratch + (long long)NPAIR * HW;
+  cudaError_t e = cudaSuccess;
+  for (int p0 = 0; p0 < NPAIR; p0 += PB) {
+    const int pb = NPAIR - p0 < PB ? NPAIR - p0 : PB;
+    dim3 gh((W + HX - 1) / HX, H);
+    k_gram_h3<NC><<<gh, HX, sizeof(float) * (NC + 1) * (HX + 2 * r), st>>>(G, hs, W, H, r, p0, pb);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    dim3 gv((W + HX - 1) / HX, (H + VROWS - 1) / VROWS, pb);
+    k_gram_v3<NC><<<gv, HX, 0, st>>>(hs, gram, W, H, r, p0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  const size_t smem = sizeof(double) * ((size_t)NPAIR * PIX + RW * 32) + sizeof(float) * (size_t)NS * PIX;
+  if ((e = cudaFuncSetAttribute(k_recur3<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  k_recur3<NC><<<(unsigned)((HW + PIX - 1) / PIX), RW * 32, smem, st>>>(gram, stats, W, H, r, lam, mode);
+  return cudaGetLastError();
+}
+
+}  // namespace st3
+}  // namespace hgf
