@@ -438,6 +438,16 @@ def main():
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         cpu = cpu_baseline(scene, c, args.cpu_sample_rows, args.cpu_sample_labels)
 
+    # whole-step bound (SURVEY 8(d) "binding roofline"): max(HBM time, fp32 time + fp64 time) of the
+    # algorithmic work at the peaks above, against the measured step (all ranks' work / N for N > 1)
+    fp32_peak = SM_COUNT * FP32_LANES * 2 * 1965e6
+    fp64_peak = SM_COUNT * FP64_LANES * 2 * 1965e6
+    t_hbm = alg_bytes(W, H, L, m) / (hbm_peak * 1e9)
+    t_alu = (fl["coef"] + fl["agg"]) * W * H * L / fp32_peak + alg_flops_stats_per_pixel(n) * W * H / fp64_peak
+    t_bound = max(t_hbm, t_alu) / world
+    binding = {"t_bound_ms": 1e3 * t_bound, "t_step_ms": ms_max / args.steps,
+               "frac": 1e3 * t_bound / (ms_max / args.steps), "bound": "alu" if t_alu > t_hbm else "hbm",
+               "basis": "max(alg bytes / HBM, alg fp32 flops / 74.4 TF + alg fp64 flops / 37.2 TF) per step"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -446,6 +456,7 @@ def main():
                 "config": config_json(c, world), "roofline": roofline,
                 "hbm": {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
                         "alg_bytes_per_step": alg_bytes(W, H, L, m)},
+                "binding_roofline": binding,
                 "stage_ms_per_step": stage_ms, "cpu_baseline": cpu, "e2e": e2e, "stereo_cost_on_gpu": stereo,
                 "segmentation": segmentation,
                 "gpu_launches": int(lt.item()), "clocks": clk}
