@@ -138,6 +138,32 @@ HGF_API hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* 
 HGF_API hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds, const uint8_t* bg_seeds,
                                int32_t* labels_out, float* min_cost_out, float* filtered_out);
 
+/* Fused WTA merge over peer memory (the compute + collective in one kernel): as
+ * hgf_aggregate_wta_prepared (statistics from hgf_prepare_rows + the caller's all-gather), but the last
+ * aggregation pass combines each pixel's packed key (hgf_aggregate_wta_ex's keys_out encoding) with a
+ * 64-bit atomic MIN directly into the key buffer of the rank that owns the pixel's row, over NVLink for a
+ * peer GPU.  peer_keys_dev: DEVICE array of `world` device pointers; peer_keys_dev[k] holds rows
+ * [k R, min(H, (k+1) R)) as int64 [R][W], R = rows_per_owner, world * R >= H (mapped with hgf_ipc_open for
+ * other processes' buffers).  Every owner buffer must hold INT64_MAX (hgf_fill_keys) before any rank starts,
+ * and is complete once every rank's call has finished on its stream (the caller synchronises, e.g. stream
+ * sync + a process-group barrier); the owner then unpacks its rows with hgf_unpack_keys_n.  Errors as
+ * hgf_aggregate_wta_prepared; HGF_ERR_UNSUPPORTED outside the k_coef3/4 + k_agg3 path. */
+HGF_API hgf_status hgf_aggregate_wta_peer(hgf_handle h, const float* cost_volume, int L, int label_offset,
+                                          int64_t* const* peer_keys_dev, int world, int rows_per_owner);
+/* keys[0 .. n) = INT64_MAX (the identity of the MIN merge), on the handle's stream. */
+HGF_API hgf_status hgf_fill_keys(hgf_handle h, int64_t* keys, long long n);
+/* hgf_unpack_keys over n contiguous keys (e.g. an owner's band of rows). */
+HGF_API hgf_status hgf_unpack_keys_n(hgf_handle h, const int64_t* keys, long long n, int32_t* labels_out,
+                                     float* min_cost_out);
+/* Device memory that can be shared with other processes (cudaMalloc) and CUDA IPC around it: handle64 is
+ * a 64-byte cudaIpcMemHandle_t; hgf_ipc_open maps another process's allocation on the current device
+ * (peer access enabled lazily), hgf_ipc_close unmaps it.  HGF_ERR_CUDA when the runtime refuses. */
+HGF_API hgf_status hgf_alloc(size_t bytes, void** dev_ptr);
+HGF_API hgf_status hgf_free(void* dev_ptr);
+HGF_API hgf_status hgf_ipc_get_handle(void* dev_ptr, unsigned char* handle64);
+HGF_API hgf_status hgf_ipc_open(const unsigned char* handle64, void** dev_ptr);
+HGF_API hgf_status hgf_ipc_close(void* dev_ptr);
+
 /* Row-sharded frame preparation.  Steps 1-2 of the path for a row band:
  * the polynomial guidance for the whole frame (cheap, needed by every slice kernel) and the
  * label-independent statistics (Prop 1 recursion, Eq4 P:143-151 with readings F1/F2) of image rows

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 __all__ = ["HGF", "HGFError", "lib", "lib_path", "MODE_HGF", "MODE_GF", "EXPORTED_SYMBOLS",
-           "merge_keys_allreduce", "shard_range", "gather_stats_rows"]
+           "merge_keys_allreduce", "shard_range", "gather_stats_rows", "PeerKeys"]
 
 MODE_HGF = 0
 MODE_GF = 1
@@ -24,6 +24,8 @@ EXPORTED_SYMBOLS = (
     "hgf_aggregate_wta", "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host",
     "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
     "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment",
+    "hgf_aggregate_wta_peer", "hgf_fill_keys", "hgf_unpack_keys_n", "hgf_alloc", "hgf_free", "hgf_ipc_get_handle",
+    "hgf_ipc_open", "hgf_ipc_close",
 )
 KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost")   # HGF_KC_* order
 
@@ -68,9 +70,19 @@ def lib():
     c_float = ctypes.c_float
     L.hgf_stereo_wta.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, vp, vp, vp, vp]
     L.hgf_segment.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.hgf_aggregate_wta_peer.argtypes = [vp, vp, c_int, c_int, vp, c_int, c_int]
+    L.hgf_fill_keys.argtypes = [vp, vp, ctypes.c_longlong]
+    L.hgf_unpack_keys_n.argtypes = [vp, vp, ctypes.c_longlong, vp, vp]
+    L.hgf_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp)]
+    L.hgf_free.argtypes = [vp]
+    L.hgf_ipc_get_handle.argtypes = [vp, ctypes.c_char_p]
+    L.hgf_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.hgf_ipc_close.argtypes = [vp]
     for name in ("hgf_create", "hgf_create_ex", "hgf_destroy", "hgf_set_stream", "hgf_filter", "hgf_aggregate_wta",
                  "hgf_aggregate_wta_ex", "hgf_unpack_keys", "hgf_aggregate_wta_host", "hgf_prepare_rows",
-                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment"):
+                 "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment",
+                 "hgf_aggregate_wta_peer", "hgf_fill_keys", "hgf_unpack_keys_n", "hgf_alloc", "hgf_free",
+                 "hgf_ipc_get_handle", "hgf_ipc_open", "hgf_ipc_close"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -226,6 +238,26 @@ class HGF:
                                       _ptr(out.get("min_cost")), _ptr(out.get("filtered"))), "hgf_segment")
         return out
 
+    def aggregate_wta_peer(self, cost_volume, peer_ptrs, world, rows_per_owner, label_offset=0):
+        """hgf_aggregate_wta_peer: the slices' keys merged by atomic MIN into the owners' buffers
+        (peer_ptrs: int64 CUDA tensor of `world` device addresses, e.g. PeerKeys.ptrs)."""
+        torch = self._torch
+        L = cost_volume.shape[0]
+        self._dev(cost_volume, (L, self.H, self.W), torch.float32, "cost_volume")
+        self._dev(peer_ptrs, (world,), torch.int64, "peer_ptrs")
+        self._bind_stream()
+        self._check(lib().hgf_aggregate_wta_peer(self._h, _ptr(cost_volume), L, int(label_offset), _ptr(peer_ptrs),
+                                                 int(world), int(rows_per_owner)), "hgf_aggregate_wta_peer")
+
+    def fill_keys(self, keys):
+        self._bind_stream()
+        self._check(lib().hgf_fill_keys(self._h, _ptr(keys), keys.numel()), "hgf_fill_keys")
+
+    def unpack_keys_n(self, keys, labels_out, min_cost_out=None):
+        self._bind_stream()
+        self._check(lib().hgf_unpack_keys_n(self._h, _ptr(keys), keys.numel(), _ptr(labels_out), _ptr(min_cost_out)),
+                    "hgf_unpack_keys_n")
+
     def prepare_rows(self, guide, y0, y1):
         """hgf_prepare_rows: guidance for the frame + statistics of rows [y0, y1)."""
         self._dev(guide, (self.m, self.H, self.W), self._torch.float32, "guide")
@@ -327,3 +359,70 @@ def gather_stats_rows(h, group=None):
             dist.broadcast(view[y0:y1].contiguous() if not view[y0:y1].is_contiguous() else view[y0:y1], src=g_src,
                            group=group)
     return view
+
+
+def _device_view(ptr, shape, typestr, device):
+    import torch
+
+    class _V:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_V(), device=device)
+
+
+class PeerKeys:
+    """Owner-partitioned key buffers for hgf_aggregate_wta_peer (the fused merge): rank k owns
+    rows [k R, min(H, (k+1) R)), R = ceil(H / world), in a cudaMalloc'd int64 [R][W] buffer; the buffers
+    are exchanged once with CUDA IPC (handles all-gathered over the process group) so that every rank's
+    aggregation kernel can atomicMin into every owner's rows over NVLink.  With world == 1 no IPC is used."""
+
+    def __init__(self, h, group=None):
+        import torch
+        import torch.distributed as dist
+        self.h, self.group = h, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.rows = -(-h.H // self.world)
+        self.y0 = self.rank * self.rows
+        self.y1 = min(h.H, self.y0 + self.rows)
+        nbytes = 8 * self.rows * h.W
+        p = ctypes.c_void_p()
+        st = lib().hgf_alloc(nbytes, ctypes.byref(p))
+        if st != 0:
+            raise HGFError(f"hgf_alloc: {lib().hgf_status_string(st).decode()}")
+        self._own = p.value
+        self._opened = []
+        ptrs = [0] * self.world
+        ptrs[self.rank] = self._own
+        if self.world > 1:
+            hd = ctypes.create_string_buffer(64)
+            st = lib().hgf_ipc_get_handle(ctypes.c_void_p(self._own), hd)
+            if st != 0:
+                self.close()
+                raise HGFError("hgf_ipc_get_handle failed")
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(hd.raw), group=group)
+            for k, raw in enumerate(handles):
+                if k == self.rank:
+                    continue
+                q = ctypes.c_void_p()
+                if lib().hgf_ipc_open(raw, ctypes.byref(q)) != 0:
+                    self.close()
+                    raise HGFError(f"hgf_ipc_open of rank {k}'s key buffer failed (no peer access?)")
+                self._opened.append(q.value)
+                ptrs[k] = q.value
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=h.device)
+        self.keys = _device_view(self._own, (self.rows, h.W), "<i8", h.device)   # this rank's rows
+
+    def reset(self):
+        """Fill this rank's rows with the MIN identity (every rank, then a barrier, before the merge)."""
+        self.h.fill_keys(self.keys)
+
+    def close(self):
+        for q in self._opened:
+            lib().hgf_ipc_close(ctypes.c_void_p(q))
+        self._opened = []
+        if getattr(self, "_own", None):
+            lib().hgf_free(ctypes.c_void_p(self._own))
+            self._own = None
+

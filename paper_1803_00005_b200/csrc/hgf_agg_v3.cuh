@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     k_agg3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ G, int W, int H, int pad, int L, int label_base, float* __restrict__ filtered_out,
            int do_wta, int first, int last, float* __restrict__ best_cost, int32_t* __restrict__ best_label,
-           int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out, int64_t* __restrict__ keys_out) {
+           int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out, int64_t* __restrict__ keys_out,
+           long long* const* __restrict__ peer_keys, int rows_per_owner) {
   using Gm = AggGeom<NC, R, IL>;
   constexpr int K = Gm::K, KA = Gm::KA, BX = Gm::BX, BY = Gm::BY, PLANE = Gm::PLANE, NV4 = Gm::NV4;
   constexpr unsigned BYTES_A = Gm::KA * PLANE * 4u, BYTES_B = Gm::KB * PLANE * 4u;
@@ -266,11 +267,18 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (labels_out) labels_out[p] = bl[s];
       if (min_cost_out) min_cost_out[p] = best[s];
       if (keys_out) keys_out[p] = pack_key_signed(best[s], bl[s]);
+      if (peer_keys) {
+        // fused merge: a 64-bit atomic MIN on the owner GPU's key buffer (over NVLink for remote owners)
+        const int owner = gy / rows_per_owner;
+        atomicMin(peer_keys[owner] + (long long)(gy - owner * rows_per_owner) * W + gx,
+                  (long long)pack_key_signed(best[s], bl[s]));
+      }
     } else {
       best_cost[p] = best[s];
       best_label[p] = bl[s];
     }
   }
+  if (last && peer_keys) __threadfence_system();
 }
 
 template <int NC, int R, bool IL>
@@ -289,7 +297,8 @@ cudaError_t agg3_launch(const void* tmaps, const AggArgs& a, cudaStream_t st) {
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
   k_agg3<NC, R, IL><<<grid, THREADS, smem, st>>>(tm[0], tm[1], a.G, a.W, a.H, a.pad, a.L, a.label_base,
                                                  a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
-                                                 a.best_label, a.labels_out, a.min_cost_out, a.keys_out);
+                                                 a.best_label, a.labels_out, a.min_cost_out, a.keys_out,
+                                                 a.peer_keys, a.rows_per_owner);
   return cudaGetLastError();
 }
 

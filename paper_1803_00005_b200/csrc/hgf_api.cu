@@ -1,6 +1,7 @@
 // C ABI of the HGF hot path (declared in include/hgf.h).  Validation, scratch ownership, stream
 // handling and launch sequencing; every step of the path runs in the kernels of hgf_kernels.cu.
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -32,6 +33,8 @@ struct hgf_ctx {
   float* sg_cost = nullptr;    // hgf_segment: the two cost slices [2][H][W]
   int* sg_counts = nullptr;    // hgf_segment: seed histograms [2][m][32] then seed counts [2]
   double* st3_scratch = nullptr;   // k_stats3 (n >= kStats3MinN): Gram planes + one batch of row sums
+  long long* const* peer_keys = nullptr;   // hgf_aggregate_wta_peer: set for the duration of the call
+  int rows_per_owner = 0;
   float* st_vol[2] = {nullptr, nullptr};
   int32_t* st_labels = nullptr;
   int st_chunk = 0;
@@ -296,6 +299,8 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
     a.labels_out = labels_out;
     a.min_cost_out = min_cost_out;
     a.keys_out = keys_out;
+    a.peer_keys = h->peer_keys;
+    a.rows_per_owner = h->rows_per_owner;
     e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
   }
@@ -595,6 +600,89 @@ hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds
   if ((s = frame_stats(h, image, 0, h->H)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out) ? 1 : 0;
   return slices(h, image, h->sg_cost, 2, 0, filtered_out, do_wta, labels_out, min_cost_out, nullptr);
+}
+
+hgf_status hgf_aggregate_wta_peer(hgf_handle h, const float* cost_volume, int L, int label_offset,
+                                  int64_t* const* peer_keys_dev, int world, int rows_per_owner) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!cost_volume || !peer_keys_dev) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
+  if (label_offset < 0 || (long long)label_offset + L > 2147483647LL)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
+  if (world < 1 || rows_per_owner < 1 || (long long)rows_per_owner * world < h->H)
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "owners must cover every row: world * rows_per_owner >= H");
+  if (!h->v3agg || !(h->v3coef || h->v4coef))
+    return fail(h, HGF_ERR_UNSUPPORTED, "the fused merge needs the k_coef3/4 + k_agg3 path");
+  hgf_status s = check_async(h);
+  if (s != HGF_OK) return s;
+  h->peer_keys = reinterpret_cast<long long* const*>(peer_keys_dev);
+  h->rows_per_owner = rows_per_owner;
+  s = slices(h, nullptr, cost_volume, L, label_offset, nullptr, 1, nullptr, nullptr, nullptr);
+  h->peer_keys = nullptr;
+  h->rows_per_owner = 0;
+  return s;
+}
+
+hgf_status hgf_fill_keys(hgf_handle h, int64_t* keys, long long n) {
+  if (!h || !keys || n < 0) return HGF_ERR_INVALID_ARGUMENT;
+  cudaError_t e = hgf::launch_fill_i64(keys, n, (long long)0x7FFFFFFFFFFFFFFFLL, h->stream);
+  return e == cudaSuccess ? HGF_OK : cuda_fail(h, e, "fill_keys");
+}
+
+hgf_status hgf_unpack_keys_n(hgf_handle h, const int64_t* keys, long long n, int32_t* labels_out,
+                             float* min_cost_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!keys || n < 0 || n > (1LL << 31) || (!labels_out && !min_cost_out))
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer or bad count");
+  cudaError_t e = traced(h, HGF_KC_KEYS, h->stream, [&] {
+    return hgf::launch_unpack_keys(keys, labels_out, min_cost_out, (int)n, 1, h->stream);
+  });
+  return e == cudaSuccess ? HGF_OK : cuda_fail(h, e, "unpack_keys");
+}
+
+hgf_status hgf_alloc(size_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes == 0) return HGF_ERR_INVALID_ARGUMENT;
+  cudaError_t e = cudaMalloc(dev_ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *dev_ptr = nullptr;
+    return e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA;
+  }
+  return HGF_OK;
+}
+
+hgf_status hgf_free(void* dev_ptr) { return cudaFree(dev_ptr) == cudaSuccess ? HGF_OK : HGF_ERR_CUDA; }
+
+hgf_status hgf_ipc_get_handle(void* dev_ptr, unsigned char* handle64) {
+  if (!dev_ptr || !handle64) return HGF_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, dev_ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return HGF_ERR_CUDA;
+  }
+  static_assert(sizeof(hd) == 64, "CUDA IPC handle size");
+  std::memcpy(handle64, &hd, 64);
+  return HGF_OK;
+}
+
+hgf_status hgf_ipc_open(const unsigned char* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return HGF_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, 64);
+  if (cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    *dev_ptr = nullptr;
+    return HGF_ERR_CUDA;
+  }
+  return HGF_OK;
+}
+
+hgf_status hgf_ipc_close(void* dev_ptr) {
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? HGF_OK : HGF_ERR_CUDA;
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {

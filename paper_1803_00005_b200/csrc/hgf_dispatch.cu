@@ -29,6 +29,11 @@ __global__ void k_unpack_keys(const int64_t* __restrict__ keys, int32_t* __restr
   }
 }
 
+__global__ void k_fill_i64(int64_t* __restrict__ p, long long n, long long v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
 // ------------------------------------------------------------------ launchers
 static int grid_1d(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
@@ -89,6 +94,12 @@ cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st) {
 #define CALL(N) agg_impl<N>(a, st)
   HGF_DISPATCH(n, CALL)
 #undef CALL
+}
+
+cudaError_t launch_fill_i64(int64_t* p, long long n, long long v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_i64<<<grid_1d(n, 256), 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_unpack_keys(const int64_t* keys, int32_t* labels, float* cost, int W, int H, cudaStream_t st) {

@@ -20,6 +20,10 @@ struct AggArgs {
   int32_t* labels_out;
   float* min_cost_out;
   int64_t* keys_out;
+  // fused WTA merge over peer memory (k_agg3 only): the last pass atomicMin's each pixel's key into the key
+  // buffer of the rank owning its row: peer_keys[gy / rows_per_owner][(gy % rows_per_owner) * W + gx]
+  long long* const* peer_keys;
+  int rows_per_owner;
 };
 
 cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st);
@@ -34,6 +38,7 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
 cudaError_t launch_coef(int n, const float* G, const float* stats, const float* vol, float* wbuf, int W, int H,
                         int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg(int n, const AggArgs& a, cudaStream_t st);
+cudaError_t launch_fill_i64(int64_t* p, long long n, long long v, cudaStream_t st);
 cudaError_t launch_unpack_keys(const int64_t* keys, int32_t* labels, float* cost, int W, int H, cudaStream_t st);
 
 }  // namespace hgf

@@ -357,3 +357,41 @@ def test_segment_two_colour_fixture_and_empty_seeds():
     with pytest.raises(HGFError):
         h.segment(gi, torch.from_numpy(fg).cuda(), torch.zeros(H, W, dtype=torch.uint8, device="cuda"))
     h.close()
+
+
+def test_peer_merge_equals_allreduce_merge():
+    """Fused WTA merge over peer memory (hgf_aggregate_wta_peer): two label shards x two row owners, run in
+    one process (the owners are plain device buffers here; across processes they are CUDA-IPC mappings):
+    the owners' rows are bit-exactly the unsharded keys, and unpack to the unsharded labels."""
+    torch = _torch()
+    from paper_1803_00005_b200 import PeerKeys, shard_range
+    W, H, L = 180, 77, 30
+    scene = synth.make_stereo_scene(W, H, L, seed=91)
+    gi = torch.from_numpy(scene.left).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    ref = h.aggregate_wta_ex(gi, vol, labels=True, keys=True)
+    # world = 1 through PeerKeys (no IPC)
+    pk = PeerKeys(h)
+    pk.reset()
+    h.prepare_rows(gi, 0, H)
+    h.aggregate_wta_peer(vol, pk.ptrs, 1, pk.rows)
+    torch.cuda.synchronize()
+    assert torch.equal(pk.keys, ref["keys"])
+    lab = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    h.unpack_keys_n(pk.keys, lab)
+    assert torch.equal(lab, ref["labels"])
+    pk.close()
+    # two owners (rows split) x two label shards
+    R = (H + 1) // 2
+    owners = [torch.empty((R, W), dtype=torch.int64, device="cuda") for _ in range(2)]
+    for o in owners:
+        h.fill_keys(o)
+    ptrs = torch.tensor([o.data_ptr() for o in owners], dtype=torch.int64, device="cuda")
+    for rank in range(2):
+        l0, l1 = shard_range(L, 2, rank)
+        h.aggregate_wta_peer(vol[l0:l1].contiguous(), ptrs, 2, R, label_offset=l0)
+    torch.cuda.synchronize()
+    merged = torch.cat(owners)[:H]
+    assert torch.equal(merged, ref["keys"])
+    h.close()
