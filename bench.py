@@ -185,7 +185,8 @@ def run_reference(args, c):
 def config_json(c, n_gpus):
     return {"workload": workload_name(c), "W": c["W"], "H": c["H"], "labels": c["L"], "n_guide": c["m"],
             "poly_degree": c["d"], "n": c["n"], "radius": c["r"], "lambda": c["lam"],
-            "parallelism": (f"labels sharded x{n_gpus} (keys allreduce-MIN), statistics rows sharded (all-gather)"
+            "parallelism": (f"labels sharded x{n_gpus} (WTA merged by atomic MIN into the row owners over NVLink, "
+                            "fallback NCCL allreduce-MIN), statistics rows sharded (NCCL all-gather)"
                             if n_gpus > 1 else "single GPU"),
             "l2": "inputs larger than L2 (cost volume > 126 MB); no flush needed"}
 
@@ -267,7 +268,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1803_00005_b200 import HGF, HGFError, gather_stats_rows, merge_keys_allreduce, shard_range
+    from paper_1803_00005_b200 import HGF, HGFError, PeerKeys, gather_stats_rows, merge_keys_allreduce, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -299,10 +300,28 @@ def main():
             row_sharded = True
         except HGFError:
             row_sharded = False
+    # fused merge (default for N > 1): the aggregation kernel atomicMin's keys into the row owners' buffers
+    # over NVLink (CUDA IPC); HGF_BENCH_MERGE=nccl keeps the allreduce-MIN baseline
+    peer = None
+    if world > 1 and row_sharded and os.environ.get("HGF_BENCH_MERGE", "peer") == "peer":
+        try:
+            peer = PeerKeys(h)
+        except Exception as ex:   # no peer mapping on this box: the NCCL merge below
+            print(f"[bench] peer merge unavailable ({ex}); using allreduce-MIN", file=sys.stderr)
+            peer = None
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    band_labels = labels[: (peer.y1 - peer.y0)] if peer is not None else None
 
     def step():
         if world == 1:
             h.aggregate_wta(guide, vol, labels)
+        elif peer is not None:
+            peer.reset()
+            h.prepare_rows(guide, y0, y1)
+            gather_stats_rows(h)          # NCCL all-gather: also orders every owner's reset before any merge
+            h.aggregate_wta_peer(vol, peer.ptrs, world, peer.rows, label_offset=l0)
+            dist.all_reduce(flag)         # every rank's atomics have landed (stream-ordered, no host sync)
+            h.unpack_keys_n(peer.keys[: peer.y1 - peer.y0], band_labels)
         elif row_sharded:
             h.prepare_rows(guide, y0, y1)
             gather_stats_rows(h)
@@ -416,7 +435,9 @@ def main():
                 vol.copy_(vol_h, non_blocking=True)
                 guide.copy_(guide_h, non_blocking=True)
                 step()
-                if rank == 0:
+                if peer is not None:          # every rank holds the labels of its own rows
+                    lab_h[: peer.y1 - peer.y0].copy_(band_labels, non_blocking=True)
+                elif rank == 0:
                     lab_h.copy_(labels, non_blocking=True)
                 torch.cuda.synchronize()
 
@@ -430,6 +451,9 @@ def main():
             e2e = {"value": W * H * L * args.e2e_steps / float(dt.item()), "unit": UNIT,
                    "h2d_bytes_per_step": 4 * W * H * L + 4 * m * W * H * world, "d2h_bytes_per_step": 4 * W * H,
                    "api": ("torch H2D copies + HGF.prepare_rows + NCCL all-gather of the statistics rows + "
+                           "HGF.aggregate_wta_peer (keys atomicMin'd into the row owners over NVLink) + "
+                           "HGF.unpack_keys_n" if peer is not None else
+                           "torch H2D copies + HGF.prepare_rows + NCCL all-gather of the statistics rows + "
                            "HGF.aggregate_wta_prepared + NCCL allreduce-MIN + HGF.unpack_keys" if row_sharded else
                            "torch H2D copies + HGF.aggregate_wta_ex + NCCL allreduce-MIN + HGF.unpack_keys")}
 
