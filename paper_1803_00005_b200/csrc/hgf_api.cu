@@ -206,7 +206,8 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
     if (h->v3coef) {
       // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 88 x 1 x 32 (k_coef3)
       CUtensorMap tm_vol;
-      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, 88, 1, 32))
+      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, 88, 1,
+                         hgf::coef3_labels(h->n)))
         return cudaErrorInvalidValue;
       return hgf::launch_coef_v3(h->n, &tm_vol, &h->tm_g, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                  h->stream);
@@ -356,7 +357,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   }
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&h->G, sizeof(float) * h->n * HW)) != cudaSuccess ||
-      (e = cudaMalloc(&h->stats, sizeof(float) * std::max(hgf::stats_planes(h->n), hgf::kStatsAos) * HW)) !=
+      (e = cudaMalloc(&h->stats, sizeof(float) * std::max(hgf::stats_planes(h->n), hgf::stats_aos_floats(h->n)) * HW)) !=
           cudaSuccess) {
     cudaGetLastError();
     release(h);
@@ -369,7 +370,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->v4coef = h->v3agg && h->n <= 6 && (W % 4) == 0 && h->r <= 9 && (f4 && f4[0] == '1') &&
                 encode_map_3d(&h->tm_g4, h->G, W, H, h->n, W, (long long)W * H, hgf::kCoef4BoxX, 1, h->n);
     const char* f = std::getenv("HGF_COEF3");
-    h->v3coef = !h->v4coef && h->v3agg && h->n <= 6 && (W % 4) == 0 && !(f && f[0] == '0') &&
+    h->v3coef = !h->v4coef && h->v3agg && h->n <= hgf::kCoef3MaxN && (W % 4) == 0 && !(f && f[0] == '0') &&
                 encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
   }
   // coefficient buffer layout: label-interleaved for k_coef3 -> k_agg3, else rows pitched to a multiple of
@@ -488,7 +489,7 @@ hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row)
   if (!(h->v3coef || h->v4coef))
     return fail(h, HGF_ERR_UNSUPPORTED, "statistics are not stored row-contiguously in this configuration");
   *dev_ptr = h->stats;
-  *bytes_per_row = sizeof(float) * (size_t)hgf::kStatsAos * h->W;
+  *bytes_per_row = sizeof(float) * (size_t)hgf::stats_aos_floats(h->n) * h->W;
   return HGF_OK;
 }
 

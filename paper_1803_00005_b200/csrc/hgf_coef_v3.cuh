@@ -35,38 +35,42 @@ namespace v3 {
 #define HGF_EXP 0   // timing experiments only: 1 = V warps alone, 2 = H warps alone, 3 = neither (wrong results)
 #endif
 constexpr int C_TX = 64;                    // owned columns per strip
-constexpr int C_LB = 32;                    // labels per CTA batch
 constexpr int C_LG = 8;                     // labels per V thread
-constexpr int C_NG = C_LB / C_LG;           // V label groups
 constexpr int C_HSEG = 16;                  // pixels per H thread (two store groups of 8)
-static_assert(C_HSEG == kWGroupPx && C_LB == kWGroupLabels, "an H segment is one group of the interleaved layout");
+static_assert(C_HSEG == kWGroupPx, "an H segment is one group of the interleaved layout");
 constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
-constexpr int C_NHW = C_LB * C_NSEG / 32;   // H warps: each = the 32 labels of one segment
 constexpr int C_RMAX = 9;
 constexpr int C_BXP = 88;                   // TMA box width: >= TX + 2*RMAX + 3 (x start rounded down to 16 B)
-constexpr int C_SPX = 28;                   // floats per pixel in the SMEM statistics row (27 + kappa)
-constexpr int C_SSEG = C_HSEG * C_SPX + 16; // segment stride: consecutive segments 16 banks apart
 constexpr int C_BAR_V = 5;                  // named barrier among the V warps
 
 template <int NC>
 struct CoefGeom {
   static constexpr int K = NC + 1, NP = NC * (NC + 1) / 2, NS = NP + NC;
-  static_assert(NS + 1 <= C_SPX, "statistics + kappa must fit the per-pixel slot");
+  // labels per CTA: 32 (H warp = one segment, lane = label) up to n = 6; 16 for n = 7..9 (H warp = two
+  // segments x 16 labels) so that the V rows of n + 1 planes still double-buffer in SMEM
+  static constexpr int LB = coef3_labels(NC);
+  static_assert(kWGroupLabels % LB == 0, "a CTA's labels lie in one 32-label group of the layout");
+  static constexpr int NG = LB / C_LG;                      // V label groups
+  static constexpr int NHW = LB * C_NSEG / 32;              // H warps
+  static constexpr int SPX = stats_aos_floats(NC);          // floats per pixel in the SMEM statistics row
+  static_assert(NS + 1 <= SPX, "statistics + kappa must fit the per-pixel slot");
+  // segment stride: consecutive segments 16 banks apart
+  static constexpr int SSEG = C_HSEG * SPX + (16 - (C_HSEG * SPX) % 32 + 32) % 32;
   static constexpr int CXMAX = C_TX + 2 * C_RMAX;         // V columns (strip + halo), max 82
   static constexpr int CP = CXMAX;                          // SMEM column pitch
   static constexpr int LSTRIDE = K * CP + ((K * CP) % 2 == 0 ? 1 : 0);  // floats per label (odd)
-  static constexpr int VROW = C_LB * LSTRIDE;               // floats per V row buffer
-  static constexpr int SROW = C_NSEG * C_SSEG;              // statistics row
-  // one TMA stage: entering + leaving rows of the 32 labels' cost slices and of the NC guidance planes
+  static constexpr int VROW = LB * LSTRIDE;                 // floats per V row buffer
+  static constexpr int SROW = C_NSEG * SSEG;                // statistics row
+  // one TMA stage: entering + leaving rows of the LB labels' cost slices and of the NC guidance planes
   // (every TMA destination 128-byte aligned: sizes rounded to 32 floats)
-  static constexpr int PROW = C_LB * C_BXP, GROW = ((NC > 0 ? NC : 1) * C_BXP + 31) / 32 * 32;
+  static constexpr int PROW = LB * C_BXP, GROW = ((NC > 0 ? NC : 1) * C_BXP + 31) / 32 * 32;
   static constexpr int STAGE = 2 * PROW + 2 * GROW;
   // per (segment, label): the 2R+1 window sums of the segment's first pixel, computed by the V warps
-  static constexpr int ISEG = C_LB * K + 16 + ((C_LB * K) % 32 == 16 ? 16 : 0);  // = 16 banks mod 32
+  static constexpr int ISEG = LB * K + 16 + ((LB * K) % 32 == 16 ? 16 : 0);  // = 16 banks mod 32
   static constexpr int INI = C_NSEG * ISEG;
   static constexpr int CXP = (CXMAX + 31) / 32 * 32;        // V threads per label group (warp-aligned groups)
-  static constexpr int NVW = (CXP * C_NG + 31) / 32;        // V warps
-  static constexpr int THREADS = (NVW + C_NHW) * 32;
+  static constexpr int NVW = (CXP * NG + 31) / 32;          // V warps
+  static constexpr int THREADS = (NVW + NHW) * 32;
   static constexpr size_t SMEM =
       sizeof(float) * (2 * (size_t)STAGE + 2 * (size_t)VROW + 2 * (size_t)SROW + 2 * (size_t)INI) + 64;
 };
@@ -95,7 +99,8 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
             int BH, float lam0) {
   using Gm = CoefGeom<NC>;
   constexpr int K = Gm::K, NP = Gm::NP, NS = Gm::NS, CP = Gm::CP, LSTRIDE = Gm::LSTRIDE;
-  constexpr int NV = Gm::NVW * 32, NH = C_NHW * 32, NALL = NV + NH;
+  constexpr int NV = Gm::NVW * 32, NH = Gm::NHW * 32, NALL = NV + NH;
+  constexpr int C_LB = Gm::LB, C_NG = Gm::NG, C_SPX = Gm::SPX, C_SSEG = Gm::SSEG;
   const int r = (R > 0) ? R : r_arg;
   extern __shared__ __align__(128) float sm[];
   float* stage = sm;                              // [2][STAGE]: pe[32][BXP], pl[32][BXP], ge[NC][BXP], gl[NC][BXP]
@@ -237,8 +242,8 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
     const int h = tid - NV, hw = h >> 5, ln = h & 31;
     // lane = label, warp = segment: each pixel's statistics are one broadcast per warp, and the odd
     // LSTRIDE keeps the 32 labels' V-row loads conflict-free
-    const int lab = ln;                               // label within the batch
-    const int seg = hw;                               // 16-pixel segment 0..3
+    const int lab = C_LB == 32 ? ln : (ln & 15);                   // label within the batch
+    const int seg = C_LB == 32 ? hw : 2 * hw + (ln >> 4);          // 16-pixel segment 0..3
     const int l = lb0 + lab;
     const bool lok = l < L;
     const int xs = seg * C_HSEG;                      // first owned pixel (strip-relative)
@@ -294,8 +299,9 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
         // labels of the half-warp cover one contiguous 1 KB run (see WLayout)
         const int grp = (x0 + xs) / kWGroupPx;
         if (lok && grp < wo.xg) {
-          float* wg = wbuf + (((long long)blockIdx.z * K * H + y) * wo.xg + grp) * (kWGroupPx * kWGroupLabels) +
-                      lab * kWGroupPx + q8;
+          float* wg = wbuf + (((long long)(l / kWGroupLabels) * K * H + y) * wo.xg + grp) *
+                                 (kWGroupPx * kWGroupLabels) +
+                      (l % kWGroupLabels) * kWGroupPx + q8;
           const long long kstride = (long long)H * wo.xg * (kWGroupPx * kWGroupLabels);
 #pragma unroll
           for (int k = 0; k < K; ++k) st_global_v8(wg + k * kstride, wv[k]);
@@ -330,7 +336,7 @@ cudaError_t coef3_r(const void* tm_vol, const void* tm_g, const float* stats, fl
   cudaError_t e = cudaFuncSetAttribute(k_coef3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
   if (e != cudaSuccess) return e;
   // band height: enough CTAs to fill 148 SMs at least ~4 times, but long enough to amortise the warm-up
-  const int strips = (W + C_TX - 1) / C_TX, batches = (L + C_LB - 1) / C_LB;
+  const int strips = (W + C_TX - 1) / C_TX, batches = (L + Gm::LB - 1) / Gm::LB;
   int BH = 128;
   while (BH > 32 && (long long)strips * ((H + BH - 1) / BH) * batches < 4 * 148) BH /= 2;
   dim3 grid(strips, (H + BH - 1) / BH, batches);

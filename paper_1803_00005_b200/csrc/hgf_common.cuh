@@ -42,7 +42,7 @@ constexpr int kWGroupPx = 16, kWGroupLabels = 32;
 // Suspend-time hint (ns) for mbarrier.try_wait: a waiting warp is parked until the phase completes (or
 // the hint elapses) instead of spinning through issue slots the working warps need.
 constexpr unsigned kMbarSuspendNs = 20000;
-// Floats per pixel record of the per-pixel ("AoS") statistics layout read by k_coef3.
+// Floats per pixel record of the per-pixel ("AoS") statistics layout read by k_coef3 / k_coef4 (n <= 6).
 constexpr int kStatsAos = 28;
 struct WLayout {
   long long origin;   // = pad * pitch + pad
@@ -55,5 +55,12 @@ struct WLayout {
 
 // Number of statistics planes stored per pixel for n channels: P' (upper triangle) + nu.
 __host__ __device__ constexpr int stats_planes(int n) { return n * (n + 1) / 2 + n; }
+// Floats per per-pixel statistics record (the statistics, then kappa, padded to 16 bytes): 28 for n <= 6.
+__host__ __device__ constexpr int stats_aos_floats(int n) {
+  return n <= 6 ? kStatsAos : (stats_planes(n) + 1 + 3) / 4 * 4;
+}
+// k_coef3: labels per CTA (32 up to n = 6; 16 for n = 7..9 so the V rows of n + 1 planes fit SMEM).
+constexpr int kCoef3MaxN = 9;
+__host__ __device__ constexpr int coef3_labels(int n) { return n <= 6 ? 32 : 16; }
 
 }  // namespace hgf

@@ -180,6 +180,7 @@ cudaError_t launch_coef_v3(int n, const void* tm_vol, const void* tm_g, const fl
 #define C3(N) return v3::coef3_impl<N>(tm_vol, tm_g, stats, wbuf, wo, W, H, r, L, lam0, st)
   switch (n) {
     case 1: C3(1); case 2: C3(2); case 3: C3(3); case 4: C3(4); case 5: C3(5); case 6: C3(6);
+    case 7: C3(7); case 8: C3(8); case 9: C3(9);
     default: return cudaErrorInvalidValue;
   }
 #undef C3

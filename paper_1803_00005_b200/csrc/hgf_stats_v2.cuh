@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
   const long long p = (long long)gy * W + gx;
   const double den = (mode == 0) ? (lam + N) : N;
   if (aos) {
-    float rec[kStatsAos];
+    constexpr int REC = stats_aos_floats(NC);
+    float rec[REC];
     int s = 0;
 #pragma unroll
     for (int a = 1; a < K; ++a)
@@ -170,10 +171,10 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
     for (int a = 1; a < K; ++a) rec[s++] = (float)(Gm[0][a] / den);
     rec[s++] = 1.0f / (lam0f + (float)N);
 #pragma unroll
-    for (; s < kStatsAos; ++s) rec[s] = 0.0f;
-    float4* o = reinterpret_cast<float4*>(stats + p * kStatsAos);
+    for (; s < REC; ++s) rec[s] = 0.0f;
+    float4* o = reinterpret_cast<float4*>(stats + p * REC);
 #pragma unroll
-    for (int q = 0; q < kStatsAos / 4; ++q) o[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+    for (int q = 0; q < REC / 4; ++q) o[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
     return;
   }
   int s = 0;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
 template <int NC>
 cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
                         int y0, int y1, cudaStream_t st) {
-  if (aos && stats_planes(NC) + 1 > kStatsAos) return cudaErrorInvalidValue;
+  if (aos && NC > kCoef3MaxN) return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(NC, r);
   cudaError_t e = cudaFuncSetAttribute(k_stats2<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

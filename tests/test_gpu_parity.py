@@ -53,6 +53,10 @@ CASES = [
     ("il-n6-L35", 100, 37, 3, 2, 35, 9, 0.05, "hgf"),
     ("il-n6-r4-gf", 132, 29, 3, 2, 33, 4, 0.05, "gf"),
     ("il-n3-r7", 68, 40, 3, 1, 40, 7, 1e-3, "hgf"),
+    # k_coef3 with 16-label CTAs and wider statistics records (n = 7..9)
+    ("il-n9", 100, 37, 3, 3, 20, 9, 0.05, "hgf"),
+    ("il-n8-gf", 132, 29, 4, 2, 17, 4, 0.05, "gf"),
+    ("il-n7", 68, 40, 7, 1, 33, 7, 1e-3, "hgf"),
 ]
 
 
@@ -234,9 +238,9 @@ def test_prepared_row_bands_equal_unsharded(monkeypatch, coef4):
 def test_prepared_path_unsupported_config_fails_loudly():
     torch = _torch()
     from paper_1803_00005_b200 import HGFError
-    h = _hgf(40, 30, 3, 3, 4, 0.05, "hgf")                  # n = 9: planar statistics, no row bands
+    h = _hgf(42, 30, 3, 2, 4, 0.05, "hgf")                  # W % 4 != 0: planar statistics, no row bands
     with pytest.raises(HGFError):
-        h.prepare_rows(torch.zeros(3, 30, 40, device="cuda"), 0, 30)
+        h.prepare_rows(torch.zeros(3, 30, 42, device="cuda"), 0, 30)
     with pytest.raises(HGFError):
         h.stats_view()
     h.close()
