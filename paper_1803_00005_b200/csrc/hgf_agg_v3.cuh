@@ -88,7 +88,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 
 // tmA / tmB: tensor maps whose box covers planes [0, KA) / [KA, K) of one slice.
 template <int NC, int R, bool IL>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 ? 2 : 1)   // 2 CTAs/SM when the tile fits twice
     k_agg3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ G, int W, int H, int pad, int L, int label_base, float* __restrict__ filtered_out,
            int do_wta, int first, int last, float* __restrict__ best_cost, int32_t* __restrict__ best_label,
