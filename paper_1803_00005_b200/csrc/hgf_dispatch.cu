@@ -62,8 +62,8 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
                          float lam0f, int y0, int y1, double* scratch3, cudaStream_t st) {
   const int TS = 16 + 2 * r;
   // = st2::smem_bytes(n, r): odd-pitch channel tiles, 17-double rows of horizontal sums, vertical sums
-  const size_t smem2 = ((size_t)(n + 1) * TS * (TS | 1) * 4 + 15) / 16 * 16 + (size_t)8 * TS * 17 * 8 +
-                       (size_t)8 * 16 * 16 * 8 + 16;
+  const size_t smem2 = ((size_t)(n + 1) * TS * (TS | 1) * 4 + 15) / 16 * 16 + (size_t)7 * TS * 17 * 8 +
+                       (size_t)7 * 16 * 16 * 8 + 16;
   // k_stats3 (Gram planes + warp-per-pixel recursion) where k_stats2 would spill heavily (n >= kStats3MinN)
   // or not fit its channel tiles in shared memory (the O(r) v1 kernel) -- measured on the C5 sweep
   if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= kStats3MinN || (n >= 7 && smem2 > 200 * 1024))) {

@@ -19,7 +19,7 @@ namespace hgf {
 namespace st2 {
 
 constexpr int T = 16;        // output tile side
-constexpr int PB = 8;        // product planes per batch
+constexpr int PB = 7;        // product planes per batch (7 x 34 rows <= 256 threads at r = 9: one H round)
 constexpr int THREADS = T * T;
 
 constexpr int HP = T + 1;     // row pitch (doubles) of the horizontal sums: lanes walk rows conflict-free
