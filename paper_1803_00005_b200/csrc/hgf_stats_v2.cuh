@@ -83,16 +83,18 @@ __global__ void __launch_bounds__(THREADS) k_stats2(const float* __restrict__ G,
       }
     }
     __syncthreads();
-    for (int item = tid; item < PB * T; item += THREADS) {
-      const int pb = item / T, col = item % T;
+    // vertical sums: two threads per (pair, column), 8 output rows each (twice the parallelism of one
+    // 16-row slide for 19 extra loads)
+    for (int item = tid; item < PB * T * 2; item += THREADS) {
+      const int pb = item / (2 * T), col = (item / 2) % T, half = item & 1;
       if (bt * PB + pb >= NPAIR) continue;
-      const double* hc = hb + pb * TS * HP + col;
+      const double* hc = hb + pb * TS * HP + col + half * (T / 2) * HP;
       double acc = 0.0;
       for (int dy = 0; dy <= 2 * r; ++dy) acc += hc[dy * HP];
-      double* vo = vb + pb * T * T + col;
+      double* vo = vb + pb * T * T + col + half * (T / 2) * T;
       vo[0] = acc;
 #pragma unroll
-      for (int y = 1; y < T; ++y) {
+      for (int y = 1; y < T / 2; ++y) {
         acc += hc[(y + 2 * r) * HP] - hc[(y - 1) * HP];
         vo[y * T] = acc;
       }
