@@ -22,6 +22,8 @@ Readings of the paper taken here (all listed in DESIGN.md §3):
   F7  B is a box SUM ("equal to the sum of its neighboring pixels"): lambda is against sums
   F9  HGF penalises the intercept w(0) (Eq7); GF (§5.1) does not (Eq15)
   F14 WTA ties resolve to the lowest label index
+  P1-P4 post-processing (NEXT-3; P:641 names it only): right-view cost, left-right check, row fill,
+      bilateral weighted median -- see the functions at the end and DESIGN.md §11d
   F18 Eq8 reads Z(q) = 1/|Omega_q| sum_{p in Omega_q} (sum_i w_p(i) G_i(q) + w_p(0))
 
 Parity pins for every function live in tests/test_oracle_*.py (run with -m "not gpu").
@@ -37,6 +39,7 @@ __all__ = [
     "hgf_filter", "hgf_filter_brute", "gf_he",
     "wta", "aggregate_wta", "pack_keys", "unpack_keys",
     "stereo_cost", "stereo_cost_brute", "segmentation_cost",
+    "stereo_cost_right", "lr_consistency", "occlusion_fill", "weighted_median_fill", "lr_postprocess",
 ]
 
 MODE_HGF = "hgf"
@@ -478,3 +481,103 @@ def segmentation_cost(image: np.ndarray, fg: np.ndarray, bg: np.ndarray, bins: i
             nll -= np.log(p[b[c]])
         out.append(nll / (m * np.log(N + bins)))
     return np.stack(out)
+
+
+# ----------------------------------------------------------------------------- post-processing
+# P:641 names the step ("post processing" of Hosni et al.'s framework) and gives nothing else; the
+# readings P1-P4 below follow Hosni et al.'s published framework: a right-view disparity
+# map from the same aggregation, a left-right consistency check, filling of inconsistent pixels from the
+# nearest consistent pixels of the row (the lower disparity: background), then a weighted median with
+# bilateral weights over the filled pixels only.
+
+def stereo_cost_right(left: np.ndarray, right: np.ndarray, L: int, l0: int = 0, alpha: float = 0.11,
+                      tau_c: float = 0.028, tau_g: float = 0.008) -> np.ndarray:
+    """Reading P1: the right view's cost of disparity d = l0 .. l0+L-1 is stereo_cost with the roles of the
+    views exchanged and the match searched at x + d:
+
+        C_R(x, y, d) = alpha min(mean_c |R_c(x,y) - L_c(x+d,y)|, tau_c) + (1-alpha) min(|dx R~(x,y) - dx L~(x+d,y)|, tau_g)
+
+    pixels with x + d >= W take the truncation value.  float64, (L, H, W)."""
+    left = left.astype(np.float64)
+    right = right.astype(np.float64)
+    _, H, W = left.shape
+    gl, gr = _gray_grad_x(left), _gray_grad_x(right)
+    trunc = alpha * tau_c + (1.0 - alpha) * tau_g
+    out = np.full((L, H, W), trunc)
+    for k in range(L):
+        d = l0 + k
+        if d >= W:
+            continue
+        col = np.abs(right[:, :, :W - d] - left[:, :, d:]).mean(axis=0)
+        grd = np.abs(gr[:, :W - d] - gl[:, d:])
+        out[k, :, :W - d] = alpha * np.minimum(col, tau_c) + (1.0 - alpha) * np.minimum(grd, tau_g)
+    return out
+
+
+def lr_consistency(dL: np.ndarray, dR: np.ndarray, tol: int = 0) -> np.ndarray:
+    """Reading P2: pixel (x, y) of the left disparity map is consistent iff its match lies inside the right
+    view, x - dL(x,y) >= 0, and the right map agrees there: |dL(x,y) - dR(x - dL(x,y), y)| <= tol.
+    dL, dR: int (H, W) disparities; returns bool (H, W)."""
+    dL = np.asarray(dL, dtype=np.int64)
+    dR = np.asarray(dR, dtype=np.int64)
+    H, W = dL.shape
+    xr = np.arange(W)[None, :] - dL
+    inside = (xr >= 0) & (xr < W)
+    rows = np.broadcast_to(np.arange(H)[:, None], (H, W))
+    match = dR[rows, np.clip(xr, 0, W - 1)]
+    return inside & (np.abs(dL - match) <= tol)
+
+
+def occlusion_fill(dL: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """Reading P3: an inconsistent pixel takes the disparity of the nearest consistent pixel to its left or
+    to its right on the same row, the lower of the two where both exist (occlusions belong to the
+    background), the one that exists otherwise; a row without any consistent pixel keeps its values.
+    Consistent pixels are unchanged.  int64 (H, W)."""
+    dL = np.asarray(dL, dtype=np.int64)
+    valid = np.asarray(valid, dtype=bool)
+    H, W = dL.shape
+    xs = np.broadcast_to(np.arange(W)[None, :], (H, W))
+    left_idx = np.maximum.accumulate(np.where(valid, xs, -1), axis=1)            # nearest valid at or left of x
+    right_idx = np.minimum.accumulate(np.where(valid, xs, W)[:, ::-1], axis=1)[:, ::-1]   # ... at or right of x
+    rows = np.broadcast_to(np.arange(H)[:, None], (H, W))
+    has_l, has_r = left_idx >= 0, right_idx < W
+    vl = np.where(has_l, dL[rows, np.clip(left_idx, 0, W - 1)], 0)
+    vr = np.where(has_r, dL[rows, np.clip(right_idx, 0, W - 1)], 0)
+    fill = np.where(has_l & has_r, np.minimum(vl, vr), np.where(has_l, vl, np.where(has_r, vr, dL)))
+    return np.where(valid, dL, fill)
+
+
+def weighted_median_fill(D: np.ndarray, valid: np.ndarray, image: np.ndarray, radius: int, sigma_s: float,
+                         sigma_c: float) -> np.ndarray:
+    """Reading P4: every inconsistent pixel p takes the weighted median of the filled map D over its
+    (2 radius + 1)^2 window, clipped at the image border, with bilateral weights
+
+        w(p, q) = exp(-|q - p|^2 / sigma_s^2 - sum_c (I_c(q) - I_c(p))^2 / sigma_c^2)
+
+    (I the guide image, channels first); the weighted median is the smallest window value d with
+    sum_{q: D(q) <= d} w(p, q) >= 1/2 sum_q w(p, q).  Consistent pixels are unchanged.  int64 (H, W)."""
+    D = np.asarray(D, dtype=np.int64)
+    img = np.asarray(image, dtype=np.float64)
+    H, W = D.shape
+    out = D.copy()
+    for y, x in zip(*np.nonzero(~np.asarray(valid, dtype=bool))):
+        y0, y1, x0, x1 = max(0, y - radius), min(H, y + radius + 1), max(0, x - radius), min(W, x + radius + 1)
+        yy, xx = np.mgrid[y0:y1, x0:x1]
+        dist2 = ((yy - y) ** 2 + (xx - x) ** 2).astype(np.float64)
+        col2 = ((img[:, y0:y1, x0:x1] - img[:, y, x][:, None, None]) ** 2).sum(axis=0)
+        w = np.exp(-dist2 / sigma_s ** 2 - col2 / sigma_c ** 2).ravel()
+        vals = D[y0:y1, x0:x1].ravel()
+        half = 0.5 * w.sum()
+        for d in np.unique(vals):                                   # ascending
+            if w[vals <= d].sum() >= half:
+                out[y, x] = d
+                break
+    return out
+
+
+def lr_postprocess(image: np.ndarray, dL: np.ndarray, dR: np.ndarray, tol: int = 0, radius: int = 9,
+                   sigma_s: float = 9.0, sigma_c: float = 0.1):
+    """P2 -> P3 -> P4 in order.  Returns (final disparity int64 (H, W), consistency mask bool (H, W))."""
+    valid = lr_consistency(dL, dR, tol)
+    filled = occlusion_fill(dL, valid)
+    return weighted_median_fill(filled, valid, image, radius, sigma_s, sigma_c), valid

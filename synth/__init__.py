@@ -6,6 +6,6 @@ structure of the paper's workloads (Middlebury-style stereo; c
 Hosni's framework as written in SPEC S:400).
 """
 from .stereo import (  # noqa: F401
-    CONFIGS, StereoScene, config, iid_volume, make_stereo_scene, stereo_cost_volume_np,
+    CONFIGS, StereoScene, config, iid_volume, make_lr_maps, make_stereo_scene, stereo_cost_volume_np,
     stereo_cost_volume_torch, smooth_guides,
 )

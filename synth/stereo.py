@@ -197,3 +197,24 @@ def smooth_guides(W: int, H: int, m: int, seed: int) -> np.ndarray:
         f += rng.normal(0, 0.01, size=f.shape)
         out[c] = np.clip((f - f.min()) / max(np.ptp(f), 1e-9), 0, 1)
     return out
+
+
+def make_lr_maps(W: int, H: int, L: int, seed: int, noise: float = 0.05):
+    """Inputs for the post-processing step alone (NEXT-3): the scene's left view, a left disparity map (the
+    ground truth with a fraction `noise` of pixels replaced by random labels) and a right disparity map
+    (the ground truth forward-warped to the right view, larger disparity wins, unmatched pixels 0, with the
+    same kind of noise).  Returns (left (3, H, W) float32, dL int32 (H, W), dR int32 (H, W))."""
+    scene = make_stereo_scene(W, H, L, seed)
+    rng = np.random.Generator(np.random.PCG64(seed + 7919))
+    gt = scene.disp.astype(np.int64)
+    dR = np.zeros((H, W), dtype=np.int64)
+    for y in range(H):
+        for x in range(W):
+            t = x - gt[y, x]
+            if t >= 0 and gt[y, x] > dR[y, t]:
+                dR[y, t] = gt[y, x]
+    dL = gt.copy()
+    for m in (dL, dR):
+        flip = rng.random((H, W)) < noise
+        m[flip] = rng.integers(0, L, size=int(flip.sum()))
+    return scene.left, dL.astype(np.int32), dR.astype(np.int32)

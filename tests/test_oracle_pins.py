@@ -396,3 +396,148 @@ def test_segmentation_two_colour_fixture_labels_regions():
     C = O.segmentation_cost(img, fg, bg)
     lab = O.wta(O.hgf_filter(img, C, 0.05, 2, 1))
     assert np.all(lab[:, :12] == 0) and np.all(lab[:, 18:] == 1)
+
+
+# ----------------------------------------------------------------------------- post-processing (NEXT-3)
+def test_stereo_cost_right_mirror_identities():
+    """P1 pinned two ways: C_R(x, d) = C_L(x + d, d) wherever x + d < W (the same pair of pixels), and the
+    right cost is the left cost of the x-mirrored views with their roles exchanged (the central difference
+    and its one-sided borders both change sign under the mirror; the truncation region maps onto x + d >= W)."""
+    rng = np.random.default_rng(21)
+    left, right = rng.random((3, 6, 13)), rng.random((3, 6, 13))
+    L, l0 = 7, 1
+    cr = O.stereo_cost_right(left, right, L, l0=l0, alpha=0.3, tau_c=0.2, tau_g=0.1)
+    cl = O.stereo_cost(left, right, L, l0=l0, alpha=0.3, tau_c=0.2, tau_g=0.1)
+    trunc = 0.3 * 0.2 + 0.7 * 0.1
+    for k in range(L):
+        d = l0 + k
+        assert np.allclose(cr[k][:, :13 - d], cl[k][:, d:], rtol=0, atol=1e-15)
+        assert np.all(cr[k][:, 13 - d:] == trunc)
+    mir = O.stereo_cost(right[:, :, ::-1], left[:, :, ::-1], L, l0=l0, alpha=0.3, tau_c=0.2, tau_g=0.1)[:, :, ::-1]
+    assert np.allclose(cr, mir, rtol=0, atol=1e-15)
+
+
+def _lr_brute(dL, dR, tol):
+    H, W = dL.shape
+    ok = np.zeros((H, W), bool)
+    for y in range(H):
+        for x in range(W):
+            t = x - int(dL[y, x])
+            ok[y, x] = 0 <= t < W and abs(int(dL[y, x]) - int(dR[y, t])) <= tol
+    return ok
+
+
+def _fill_brute(dL, valid):
+    H, W = dL.shape
+    out = np.array(dL, dtype=np.int64)
+    for y in range(H):
+        for x in range(W):
+            if valid[y, x]:
+                continue
+            lv = next((int(dL[y, t]) for t in range(x - 1, -1, -1) if valid[y, t]), None)
+            rv = next((int(dL[y, t]) for t in range(x + 1, W) if valid[y, t]), None)
+            if lv is not None and rv is not None:
+                out[y, x] = min(lv, rv)
+            elif lv is not None or rv is not None:
+                out[y, x] = lv if lv is not None else rv
+    return out
+
+
+def test_lr_consistency_cases():
+    """P2: brute force on random maps (tolerance 0 and 1); a constant-disparity pair is consistent exactly
+    where the match lies inside the right view (x >= d); a disparity pointing left of column 0 never is."""
+    rng = np.random.default_rng(22)
+    dL, dR = rng.integers(0, 4, (7, 15)), rng.integers(0, 4, (7, 15))
+    for tol in (0, 1, 3):
+        assert np.array_equal(O.lr_consistency(dL, dR, tol), _lr_brute(dL, dR, tol))
+    assert O.lr_consistency(dL, dR, 3)[:, 3:].all()
+    d = np.full((4, 10), 3)
+    v = O.lr_consistency(d, d)
+    assert not v[:, :3].any() and v[:, 3:].all()
+    assert not O.lr_consistency(np.array([[5, 5]]), np.array([[5, 5]]), tol=100).any()
+
+
+def test_occlusion_fill_cases():
+    """P3: hand-worked rows and brute force."""
+    X = 0
+    d = np.array([[7, X, X, 3, 9, X, 5, X]])
+    v = np.array([[1, 0, 0, 1, 1, 0, 1, 0]], bool)
+    assert O.occlusion_fill(d, v).tolist() == [[7, 3, 3, 3, 9, 5, 5, 5]]
+    assert O.occlusion_fill(np.array([[4, 8, 6]]), np.array([[0, 0, 1]], bool)).tolist() == [[6, 6, 6]]
+    assert O.occlusion_fill(np.array([[4, 8, 6]]), np.zeros((1, 3), bool)).tolist() == [[4, 8, 6]]   # no anchor
+    rng = np.random.default_rng(23)
+    dL = rng.integers(0, 30, (9, 21))
+    valid = rng.random((9, 21)) < 0.4
+    valid[3] = False
+    assert np.array_equal(O.occlusion_fill(dL, valid), _fill_brute(dL, valid))
+
+
+def test_weighted_median_special_cases():
+    """P4: with every weight equal (sigma_s, sigma_c -> inf) the weighted median is the lower median of the
+    clipped window, sorted(values)[ceil(n/2) - 1]; a dominant colour class decides alone; consistent pixels
+    are unchanged."""
+    rng = np.random.default_rng(24)
+    H, W, r = 9, 12, 2
+    D = rng.integers(0, 20, (H, W))
+    valid = rng.random((H, W)) < 0.5
+    img = rng.random((3, H, W))
+    out = O.weighted_median_fill(D, valid, img, r, 1e12, 1e12)
+    for y in range(H):
+        for x in range(W):
+            if valid[y, x]:
+                assert out[y, x] == D[y, x]
+                continue
+            win = np.sort(D[max(0, y - r):y + r + 1, max(0, x - r):x + r + 1].ravel())
+            assert out[y, x] == win[(len(win) + 1) // 2 - 1]
+    # two colours: the pixels sharing p's colour carry all the weight at small sigma_c
+    img2 = np.zeros((1, H, W))
+    img2[0, :, 6:] = 1.0
+    D2 = np.where(np.arange(W)[None, :] < 6, 3, 11) + 0 * D
+    D2[4, 2] = 11                                     # a wrong value inside the dark region
+    v2 = np.ones((H, W), bool)
+    v2[4, 2] = False
+    out2 = O.weighted_median_fill(D2, v2, img2, 3, 1e12, 0.05)
+    assert out2[4, 2] == 3
+
+
+def test_weighted_median_matches_explicit_sum():
+    """P4 against an explicit double loop over the window and an explicit threshold search."""
+    rng = np.random.default_rng(25)
+    H, W, r, ss, sc = 7, 9, 2, 2.5, 0.3
+    D = rng.integers(0, 6, (H, W))
+    valid = rng.random((H, W)) < 0.6
+    img = rng.random((2, H, W))
+    out = O.weighted_median_fill(D, valid, img, r, ss, sc)
+    for y in range(H):
+        for x in range(W):
+            if valid[y, x]:
+                continue
+            acc = {}
+            for qy in range(max(0, y - r), min(H, y + r + 1)):
+                for qx in range(max(0, x - r), min(W, x + r + 1)):
+                    c2 = sum((img[c, qy, qx] - img[c, y, x]) ** 2 for c in range(2))
+                    wq = np.exp(-((qy - y) ** 2 + (qx - x) ** 2) / ss ** 2 - c2 / sc ** 2)
+                    acc[int(D[qy, qx])] = acc.get(int(D[qy, qx]), 0.0) + wq
+            tot, run, med = sum(acc.values()), 0.0, None
+            for d in sorted(acc):
+                run += acc[d]
+                if run >= 0.5 * tot:
+                    med = d
+                    break
+            assert out[y, x] == med
+
+
+def test_lr_postprocess_improves_synthetic_stereo():
+    """End to end on a synthetic scene: the post-processed map has fewer bad pixels than the raw left map,
+    consistent pixels keep their raw disparity, and every output is a disparity of the label range."""
+    import synth
+    W, H, L = 72, 48, 16
+    scene = synth.make_stereo_scene(W, H, L, seed=31)
+    dL = O.wta(O.hgf_filter(scene.left, O.stereo_cost(scene.left, scene.right, L), 0.05, 4, 1))
+    dR = O.wta(O.hgf_filter(scene.right, O.stereo_cost_right(scene.left, scene.right, L), 0.05, 4, 1))
+    final, valid = O.lr_postprocess(scene.left, dL, dR, radius=4, sigma_s=4.0)
+    assert np.array_equal(final[valid], dL[valid])
+    assert final.min() >= 0 and final.max() < L
+    bad_raw = np.mean(np.abs(dL - scene.disp) > 1)
+    bad_pp = np.mean(np.abs(final - scene.disp) > 1)
+    assert 0.0 < valid.mean() < 1.0 and bad_pp < bad_raw
