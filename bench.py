@@ -219,10 +219,46 @@ def stereo_leg(h, scene, L, W, H, args, torch):
         lab_h.copy_(lab, non_blocking=True)
         torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
+    post = postprocess_leg(h, left, right, lab, L, W, H, args, torch)
     return {"value": W * H * L / (dev_ms / 1e3), "ms_per_step": dev_ms, "unit": UNIT,
             "e2e": {"value": W * H * L / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * left_h.numel() * 4,
                     "d2h_bytes_per_step": lab_h.numel() * 4},
-            "api": "hgf_stereo_wta (SURVEY 8(f) NEXT-2: S:400 cost slices built per chunk on the GPU)"}
+            "api": "hgf_stereo_wta (SURVEY 8(f) NEXT-2: S:400 cost slices built per chunk on the GPU)",
+            "postprocess": post}
+
+
+def postprocess_leg(h, left, right, lab, L, W, H, args, torch):
+    """NEXT-3 (hgf_stereo_disparity = left map + right map + readings P2-P4): device ms of the
+    whole pipeline per frame, and of hgf_lr_postprocess alone on this frame's two maps (defaults rho = 9,
+    sigma_s = 9, sigma_c = 0.1)."""
+    dev = left.device
+    disp = torch.empty((H, W), dtype=torch.int32, device=dev)
+    dR = h.stereo_wta_right(left, right, L)["labels"]
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {"disp": disp, "valid": torch.empty((H, W), dtype=torch.uint8, device=dev)}
+    for _ in range(3):
+        h.lr_postprocess(left, lab, dR, out=out)
+    torch.cuda.synchronize()
+    reps = 20
+    e0.record(st)
+    for _ in range(reps):
+        h.lr_postprocess(left, lab, dR, out=out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    pp_ms = e0.elapsed_time(e1) / reps
+    invalid = 1.0 - float(out["valid"].float().mean())
+    steps = max(1, min(args.steps, 5))
+    h.stereo_disparity(left, right, L, out={"disp": disp})
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        h.stereo_disparity(left, right, L, out={"disp": disp})
+    e1.record(st)
+    torch.cuda.synchronize()
+    return {"pipeline_ms_per_frame": e0.elapsed_time(e1) / steps, "postprocess_ms": pp_ms,
+            "inconsistent_fraction": invalid,
+            "api": "hgf_stereo_disparity / hgf_lr_postprocess (SURVEY 8(f) NEXT-3)"}
 
 
 def segment_leg(args, torch):

@@ -127,6 +127,44 @@ HGF_API hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* 
                                   float alpha, float tau_color, float tau_grad, int32_t* labels_out,
                                   float* min_cost_out, float* filtered_out, int64_t* keys_out);
 
+/* Right-view stereo aggregation (reading P1 of DESIGN.md §11d; P:641 names the
+ * post-processing of Hosni et al.'s framework, which needs the right view's disparity map): as
+ * hgf_stereo_wta with the right view as the guide and the views' roles exchanged, the match searched at
+ * x + d:  C_R(x,y,d) = alpha min(mean_c |R_c(x,y) - L_c(x+d,y)|, tau_color)
+ *                    + (1 - alpha) min(|dx Rbar(x,y) - dx Lbar(x+d,y)|, tau_grad),  x + d >= W -> truncation.
+ * Arguments, outputs and errors as hgf_stereo_wta (the views are still passed left, right). */
+HGF_API hgf_status hgf_stereo_wta_right(hgf_handle h, const float* left, const float* right, int L,
+                                        int label_offset, float alpha, float tau_color, float tau_grad,
+                                        int32_t* labels_out, float* min_cost_out, float* filtered_out,
+                                        int64_t* keys_out);
+
+/* Post-processing of a left disparity map (readings P2-P4 of DESIGN.md §11d, the
+ * paper only names the step):
+ *   P2  (x,y) is consistent iff x - dL >= 0 and |dL(x,y) - dR(x - dL(x,y), y)| <= tol;
+ *   P3  an inconsistent pixel takes the lower disparity of the nearest consistent pixels to its left and
+ *       right on its row (the one that exists at a border; unchanged on a row without any);
+ *   P4  then the weighted median of the filled map over its (2 radius + 1)^2 window (clipped at the border):
+ *       the smallest window value d with sum_{D(q) <= d} w >= 1/2 sum w,
+ *       w = exp(-|q - p|^2 / sigma_s^2 - |I(q) - I(p)|^2 / sigma_c^2), float32 weights.
+ * Consistent pixels keep dL.  image: device [n_guide][H][W] f32 (the handle's n_guide channels; the left
+ * view for stereo); disp_left, disp_right: device int32 [H][W] disparities; valid_out: device u8 [H][W]
+ * (1 = consistent) or NULL; disp_out: device int32 [H][W] (must not alias disp_right).  Library scratch
+ * (12 bytes per pixel) is allocated on first use.  HGF_ERR_INVALID_ARGUMENT for null pointers, tol < 0,
+ * radius outside [0, 15], non-positive or non-finite sigmas. */
+HGF_API hgf_status hgf_lr_postprocess(hgf_handle h, const float* image, const int32_t* disp_left,
+                                      const int32_t* disp_right, int tol, int radius, float sigma_s,
+                                      float sigma_c, uint8_t* valid_out, int32_t* disp_out);
+
+/* The whole stereo disparity pipeline of Hosni et al.'s framework on the GPU: hgf_stereo_wta
+ * (left map), hgf_stereo_wta_right (right map), hgf_lr_postprocess (left view as the image).  Cost and
+ * post-processing arguments as there; disparities are label_offset + label.  disp_left_out,
+ * disp_right_out (raw maps) and valid_out may be NULL; disp_out (the final map) may not.  Launches run on
+ * the handle's stream; nothing is read back. */
+HGF_API hgf_status hgf_stereo_disparity(hgf_handle h, const float* left, const float* right, int L,
+                                        int label_offset, float alpha, float tau_color, float tau_grad, int tol,
+                                        int radius, float sigma_s, float sigma_c, int32_t* disp_left_out,
+                                        int32_t* disp_right_out, uint8_t* valid_out, int32_t* disp_out);
+
 /* Foreground / background segmentation (cost form of SPEC S:406-409):
  * two cost slices (label 0 = foreground, 1 = background) from per-class, per-channel 32-bin histograms of
  * the seed pixels' colours, Laplace-smoothed: p_c(b) = (count_c(b) + 1) / (N_c + 32), cost
@@ -205,7 +243,8 @@ enum {
   HGF_KC_AGG = 3,      /* K4b per-slice aggregation Z + WTA      */
   HGF_KC_KEYS = 4,     /* key unpacking                          */
   HGF_KC_COST = 5,     /* stereo cost construction (hgf_stereo_wta) */
-  HGF_KC_COUNT = 6
+  HGF_KC_POST = 6,     /* post-processing (hgf_lr_postprocess)   */
+  HGF_KC_COUNT = 7
 };
 
 /* Tracing: when enable != 0, every kernel launch of this handle is bracketed by CUDA events recorded

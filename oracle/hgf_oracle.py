@@ -39,7 +39,7 @@ __all__ = [
     "hgf_filter", "hgf_filter_brute", "gf_he",
     "wta", "aggregate_wta", "pack_keys", "unpack_keys",
     "stereo_cost", "stereo_cost_brute", "segmentation_cost",
-    "stereo_cost_right", "lr_consistency", "occlusion_fill", "weighted_median_fill", "lr_postprocess",
+    "stereo_cost_right", "lr_consistency", "occlusion_fill", "window_weights", "weighted_median_fill", "lr_postprocess",
 ]
 
 MODE_HGF = "hgf"
@@ -547,26 +547,33 @@ def occlusion_fill(dL: np.ndarray, valid: np.ndarray) -> np.ndarray:
     return np.where(valid, dL, fill)
 
 
-def weighted_median_fill(D: np.ndarray, valid: np.ndarray, image: np.ndarray, radius: int, sigma_s: float,
-                         sigma_c: float) -> np.ndarray:
-    """Reading P4: every inconsistent pixel p takes the weighted median of the filled map D over its
-    (2 radius + 1)^2 window, clipped at the image border, with bilateral weights
+def window_weights(D: np.ndarray, image: np.ndarray, y: int, x: int, radius: int, sigma_s: float,
+                   sigma_c: float):
+    """Reading P4's window at pixel (y, x): the values D(q) and bilateral weights
 
         w(p, q) = exp(-|q - p|^2 / sigma_s^2 - sum_c (I_c(q) - I_c(p))^2 / sigma_c^2)
 
-    (I the guide image, channels first); the weighted median is the smallest window value d with
-    sum_{q: D(q) <= d} w(p, q) >= 1/2 sum_q w(p, q).  Consistent pixels are unchanged.  int64 (H, W)."""
-    D = np.asarray(D, dtype=np.int64)
+    over the (2 radius + 1)^2 window clipped at the image border (I channels first).  Returns
+    (values int64 (n,), weights float64 (n,))."""
     img = np.asarray(image, dtype=np.float64)
     H, W = D.shape
+    y0, y1, x0, x1 = max(0, y - radius), min(H, y + radius + 1), max(0, x - radius), min(W, x + radius + 1)
+    yy, xx = np.mgrid[y0:y1, x0:x1]
+    dist2 = ((yy - y) ** 2 + (xx - x) ** 2).astype(np.float64)
+    col2 = ((img[:, y0:y1, x0:x1] - img[:, y, x][:, None, None]) ** 2).sum(axis=0)
+    w = np.exp(-dist2 / sigma_s ** 2 - col2 / sigma_c ** 2).ravel()
+    return np.asarray(D[y0:y1, x0:x1], dtype=np.int64).ravel(), w
+
+
+def weighted_median_fill(D: np.ndarray, valid: np.ndarray, image: np.ndarray, radius: int, sigma_s: float,
+                         sigma_c: float) -> np.ndarray:
+    """Reading P4: every inconsistent pixel p takes the weighted median of the filled map D over its window
+    (window_weights): the smallest window value d with sum_{q: D(q) <= d} w(p, q) >= 1/2 sum_q w(p, q).
+    Consistent pixels are unchanged.  int64 (H, W)."""
+    D = np.asarray(D, dtype=np.int64)
     out = D.copy()
     for y, x in zip(*np.nonzero(~np.asarray(valid, dtype=bool))):
-        y0, y1, x0, x1 = max(0, y - radius), min(H, y + radius + 1), max(0, x - radius), min(W, x + radius + 1)
-        yy, xx = np.mgrid[y0:y1, x0:x1]
-        dist2 = ((yy - y) ** 2 + (xx - x) ** 2).astype(np.float64)
-        col2 = ((img[:, y0:y1, x0:x1] - img[:, y, x][:, None, None]) ** 2).sum(axis=0)
-        w = np.exp(-dist2 / sigma_s ** 2 - col2 / sigma_c ** 2).ravel()
-        vals = D[y0:y1, x0:x1].ravel()
+        vals, w = window_weights(D, image, y, x, radius, sigma_s, sigma_c)
         half = 0.5 * w.sum()
         for d in np.unique(vals):                                   # ascending
             if w[vals <= d].sum() >= half:

@@ -25,9 +25,9 @@ EXPORTED_SYMBOLS = (
     "hgf_last_launch_count", "hgf_status_string", "hgf_last_error", "hgf_set_profiling", "hgf_profile_read",
     "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment",
     "hgf_aggregate_wta_peer", "hgf_fill_keys", "hgf_unpack_keys_n", "hgf_alloc", "hgf_free", "hgf_ipc_get_handle",
-    "hgf_ipc_open", "hgf_ipc_close",
+    "hgf_ipc_open", "hgf_ipc_close", "hgf_stereo_wta_right", "hgf_lr_postprocess", "hgf_stereo_disparity",
 )
-KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost")   # HGF_KC_* order
+KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost", "post")   # HGF_KC_* order
 
 _lib = None
 
@@ -69,6 +69,10 @@ def lib():
     L.hgf_aggregate_wta_prepared.argtypes = [vp, vp, c_int, c_int, vp, vp, vp, vp]
     c_float = ctypes.c_float
     L.hgf_stereo_wta.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, vp, vp, vp, vp]
+    L.hgf_stereo_wta_right.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, vp, vp, vp, vp]
+    L.hgf_lr_postprocess.argtypes = [vp, vp, vp, vp, c_int, c_int, c_float, c_float, vp, vp]
+    L.hgf_stereo_disparity.argtypes = [vp, vp, vp, c_int, c_int, c_float, c_float, c_float, c_int, c_int, c_float,
+                                       c_float, vp, vp, vp, vp]
     L.hgf_segment.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.hgf_aggregate_wta_peer.argtypes = [vp, vp, c_int, c_int, vp, c_int, c_int]
     L.hgf_fill_keys.argtypes = [vp, vp, ctypes.c_longlong]
@@ -222,6 +226,64 @@ class HGF:
                                          float(tau_color), float(tau_grad), _ptr(out.get("labels")),
                                          _ptr(out.get("min_cost")), _ptr(out.get("filtered")), _ptr(out.get("keys"))),
                     "hgf_stereo_wta")
+        return out
+
+    def stereo_wta_right(self, left, right, L, label_offset=0, alpha=0.11, tau_color=0.028, tau_grad=0.008,
+                         labels=True, min_cost=False, filtered=False, keys=False, out=None):
+        """hgf_stereo_wta_right: the right view's disparity map (reading P1: right view as guide, match at
+        x + d).  Views are passed left, right as for stereo_wta."""
+        torch = self._torch
+        self._dev(left, (3, self.H, self.W), torch.float32, "left")
+        self._dev(right, (3, self.H, self.W), torch.float32, "right")
+        out = self._outputs(int(L), labels, min_cost, filtered, keys, out)
+        self._bind_stream()
+        self._check(lib().hgf_stereo_wta_right(self._h, _ptr(left), _ptr(right), int(L), int(label_offset),
+                                               float(alpha), float(tau_color), float(tau_grad),
+                                               _ptr(out.get("labels")), _ptr(out.get("min_cost")),
+                                               _ptr(out.get("filtered")), _ptr(out.get("keys"))),
+                    "hgf_stereo_wta_right")
+        return out
+
+    def lr_postprocess(self, image, disp_left, disp_right, tol=0, radius=9, sigma_s=9.0, sigma_c=0.1,
+                       valid=False, out=None):
+        """hgf_lr_postprocess (readings P2-P4): returns {"disp": int32 (H, W)[, "valid": uint8 (H, W)]}."""
+        torch = self._torch
+        self._dev(image, (self.m, self.H, self.W), torch.float32, "image")
+        self._dev(disp_left, (self.H, self.W), torch.int32, "disp_left")
+        self._dev(disp_right, (self.H, self.W), torch.int32, "disp_right")
+        out = dict(out or {})
+        dev = image.device
+        if "disp" not in out:
+            out["disp"] = torch.empty((self.H, self.W), dtype=torch.int32, device=dev)
+        if valid and "valid" not in out:
+            out["valid"] = torch.empty((self.H, self.W), dtype=torch.uint8, device=dev)
+        self._bind_stream()
+        self._check(lib().hgf_lr_postprocess(self._h, _ptr(image), _ptr(disp_left), _ptr(disp_right), int(tol),
+                                             int(radius), float(sigma_s), float(sigma_c), _ptr(out.get("valid")),
+                                             _ptr(out["disp"])), "hgf_lr_postprocess")
+        return out
+
+    def stereo_disparity(self, left, right, L, label_offset=0, alpha=0.11, tau_color=0.028, tau_grad=0.008, tol=0,
+                         radius=9, sigma_s=9.0, sigma_c=0.1, raw=False, valid=False, out=None):
+        """hgf_stereo_disparity: left map, right map, post-processing.  Returns {"disp"[, "disp_left",
+        "disp_right"][, "valid"]} (int32 / uint8 (H, W) CUDA tensors)."""
+        torch = self._torch
+        self._dev(left, (3, self.H, self.W), torch.float32, "left")
+        self._dev(right, (3, self.H, self.W), torch.float32, "right")
+        out = dict(out or {})
+        dev = left.device
+        names = ["disp"] + (["disp_left", "disp_right"] if raw else [])
+        for k in names:
+            if k not in out:
+                out[k] = torch.empty((self.H, self.W), dtype=torch.int32, device=dev)
+        if valid and "valid" not in out:
+            out["valid"] = torch.empty((self.H, self.W), dtype=torch.uint8, device=dev)
+        self._bind_stream()
+        self._check(lib().hgf_stereo_disparity(self._h, _ptr(left), _ptr(right), int(L), int(label_offset),
+                                               float(alpha), float(tau_color), float(tau_grad), int(tol), int(radius),
+                                               float(sigma_s), float(sigma_c), _ptr(out.get("disp_left")),
+                                               _ptr(out.get("disp_right")), _ptr(out.get("valid")),
+                                               _ptr(out["disp"])), "hgf_stereo_disparity")
         return out
 
     def segment(self, image, fg_seeds, bg_seeds, labels=True, min_cost=False, filtered=False, out=None):

@@ -32,6 +32,8 @@ struct hgf_ctx {
   float* sv_cost = nullptr;    // hgf_stereo_wta: one chunk of constructed cost slices [lcap][H][W]
   float* sg_cost = nullptr;    // hgf_segment: the two cost slices [2][H][W]
   int* sg_counts = nullptr;    // hgf_segment: seed histograms [2][m][32] then seed counts [2]
+  int* pp_int = nullptr;       // post-processing: filled map [H][W], then left / right disparity maps [2][H][W]
+  uint8_t* pp_valid = nullptr; // post-processing: consistency flags [H][W] (when the caller passes none)
   double* st3_scratch = nullptr;   // k_stats3 (n >= kStats3MinN): Gram planes + one batch of row sums
   long long* const* peer_keys = nullptr;   // hgf_aggregate_wta_peer: set for the duration of the call
   int rows_per_owner = 0;
@@ -127,6 +129,8 @@ void release(hgf_ctx* h) {
   cudaFree(h->sv_cost);
   cudaFree(h->sg_cost);
   cudaFree(h->sg_counts);
+  cudaFree(h->pp_int);
+  cudaFree(h->pp_valid);
   cudaFree(h->st3_scratch);
   cudaFree(h->st_vol[0]);
   cudaFree(h->st_vol[1]);
@@ -512,14 +516,17 @@ hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, in
   return slices(h, nullptr, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
 }
 
-hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, int L, int label_offset,
-                          float alpha, float tau_color, float tau_grad, int32_t* labels_out, float* min_cost_out,
-                          float* filtered_out, int64_t* keys_out) {
-  if (!h) return HGF_ERR_INVALID_ARGUMENT;
-  h->launches = 0;
-  h->err.clear();
-  if (!left || !right) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null view pointer");
-  if (h->m != 3) return fail(h, HGF_ERR_INVALID_ARGUMENT, "hgf_stereo_wta needs a 3-channel guide (the left view)");
+}  // extern "C"
+
+namespace {
+
+// hgf_stereo_wta (dir = +1: guide = left view, match at x - d) and hgf_stereo_wta_right (dir = -1: guide =
+// right view, match at x + d, reading P1).  `base` is the guide view, `other` the searched one.
+hgf_status stereo_impl(hgf_ctx* h, const float* base, const float* other, int dir, int L, int label_offset,
+                       float alpha, float tau_color, float tau_grad, int32_t* labels_out, float* min_cost_out,
+                       float* filtered_out, int64_t* keys_out) {
+  if (!base || !other) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null view pointer");
+  if (h->m != 3) return fail(h, HGF_ERR_INVALID_ARGUMENT, "stereo needs a 3-channel guide (n_guide = 3)");
   if (L < 1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "L must be >= 1");
   if (label_offset < 0 || (long long)label_offset + L > 2147483647LL)
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
@@ -541,22 +548,125 @@ hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, i
   }
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
-  if ((s = frame_stats(h, left, 0, h->H)) != HGF_OK) return s;
+  if ((s = frame_stats(h, base, 0, h->H)) != HGF_OK) return s;
   e = traced(h, HGF_KC_COST, h->stream, [&] {
-    cudaError_t e2 = hgf::launch_stereo_grad(left, h->sv_grad, h->W, h->H, h->stream);
-    return e2 != cudaSuccess ? e2 : hgf::launch_stereo_grad(right, h->sv_grad + HW, h->W, h->H, h->stream);
+    cudaError_t e2 = hgf::launch_stereo_grad(base, h->sv_grad, h->W, h->H, h->stream);
+    return e2 != cudaSuccess ? e2 : hgf::launch_stereo_grad(other, h->sv_grad + HW, h->W, h->H, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stereo gradients");
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
-  return slices_impl(h, left, nullptr, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out,
+  return slices_impl(h, base, nullptr, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out,
                      [&](int c0, int Lc, const float** chunk) {
                        *chunk = h->sv_cost;
                        return traced(h, HGF_KC_COST, h->stream, [&] {
-                         return hgf::launch_stereo_cost(left, right, h->sv_grad, h->sv_grad + HW, h->sv_cost, h->W,
-                                                        h->H, label_offset + c0, Lc, alpha, tau_color, tau_grad,
+                         return hgf::launch_stereo_cost(base, other, h->sv_grad, h->sv_grad + HW, h->sv_cost, h->W,
+                                                        h->H, label_offset + c0, Lc, dir, alpha, tau_color, tau_grad,
                                                         h->stream);
                        });
                      });
+}
+
+hgf_status pp_scratch(hgf_ctx* h) {
+  const size_t HW = (size_t)h->W * h->H;
+  cudaError_t e;
+  if (!h->pp_int) {
+    if ((e = cudaMalloc(&h->pp_int, sizeof(int32_t) * 3 * HW)) != cudaSuccess ||
+        (e = cudaMalloc(&h->pp_valid, HW)) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(h->pp_int);
+      h->pp_int = nullptr;
+      return fail(h, e == cudaErrorMemoryAllocation ? HGF_ERR_OUT_OF_MEMORY : HGF_ERR_CUDA,
+                  "post-processing scratch allocation");
+    }
+  }
+  return HGF_OK;
+}
+
+// Readings P2-P4 on device maps (the caller has checked the arguments).
+hgf_status postprocess_impl(hgf_ctx* h, const float* image, const int32_t* dL, const int32_t* dR, int tol, int radius,
+                            float sigma_s, float sigma_c, uint8_t* valid_out, int32_t* disp_out) {
+  hgf_status s = pp_scratch(h);
+  if (s != HGF_OK) return s;
+  cudaError_t e;
+  uint8_t* valid = valid_out ? valid_out : h->pp_valid;
+  int* fill = h->pp_int;
+  e = traced(h, HGF_KC_POST, h->stream, [&] {
+    cudaError_t e2 = hgf::launch_lr_fill(dL, dR, h->W, h->H, tol, valid, fill, h->stream);
+    return e2 != cudaSuccess ? e2
+                             : hgf::launch_wmf(fill, valid, image, h->m, h->W, h->H, radius, sigma_s, sigma_c, disp_out,
+                                               h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "post-processing");
+  return HGF_OK;
+}
+
+hgf_status check_pp_args(hgf_ctx* h, int tol, int radius, float sigma_s, float sigma_c) {
+  if (tol < 0) return fail(h, HGF_ERR_INVALID_ARGUMENT, "tol must be >= 0");
+  if (radius < 0 || radius > hgf::lr_wmf_max_radius())
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "weighted-median radius must be in [0, 15]");
+  if (!(sigma_s > 0.0f) || !(sigma_c > 0.0f) || !std::isfinite(sigma_s) || !std::isfinite(sigma_c))
+    return fail(h, HGF_ERR_INVALID_ARGUMENT, "sigma_s and sigma_c must be finite and > 0");
+  return HGF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, int L, int label_offset,
+                          float alpha, float tau_color, float tau_grad, int32_t* labels_out, float* min_cost_out,
+                          float* filtered_out, int64_t* keys_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  return stereo_impl(h, left, right, +1, L, label_offset, alpha, tau_color, tau_grad, labels_out, min_cost_out,
+                     filtered_out, keys_out);
+}
+
+hgf_status hgf_stereo_wta_right(hgf_handle h, const float* left, const float* right, int L, int label_offset,
+                                float alpha, float tau_color, float tau_grad, int32_t* labels_out,
+                                float* min_cost_out, float* filtered_out, int64_t* keys_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  return stereo_impl(h, right, left, -1, L, label_offset, alpha, tau_color, tau_grad, labels_out, min_cost_out,
+                     filtered_out, keys_out);
+}
+
+hgf_status hgf_lr_postprocess(hgf_handle h, const float* image, const int32_t* disp_left, const int32_t* disp_right,
+                              int tol, int radius, float sigma_s, float sigma_c, uint8_t* valid_out,
+                              int32_t* disp_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!image || !disp_left || !disp_right || !disp_out) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null pointer");
+  hgf_status s = check_pp_args(h, tol, radius, sigma_s, sigma_c);
+  if (s != HGF_OK) return s;
+  if ((s = check_async(h)) != HGF_OK) return s;
+  return postprocess_impl(h, image, disp_left, disp_right, tol, radius, sigma_s, sigma_c, valid_out, disp_out);
+}
+
+hgf_status hgf_stereo_disparity(hgf_handle h, const float* left, const float* right, int L, int label_offset,
+                                float alpha, float tau_color, float tau_grad, int tol, int radius, float sigma_s,
+                                float sigma_c, int32_t* disp_left_out, int32_t* disp_right_out, uint8_t* valid_out,
+                                int32_t* disp_out) {
+  if (!h) return HGF_ERR_INVALID_ARGUMENT;
+  h->launches = 0;
+  h->err.clear();
+  if (!disp_out) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null disp_out");
+  hgf_status s = check_pp_args(h, tol, radius, sigma_s, sigma_c);
+  if (s != HGF_OK) return s;
+  const size_t HW = (size_t)h->W * h->H;
+  if ((s = pp_scratch(h)) != HGF_OK) return s;
+  int32_t* dL = disp_left_out ? disp_left_out : h->pp_int + HW;
+  int32_t* dR = disp_right_out ? disp_right_out : h->pp_int + 2 * HW;
+  if ((s = stereo_impl(h, left, right, +1, L, label_offset, alpha, tau_color, tau_grad, dL, nullptr, nullptr,
+                       nullptr)) != HGF_OK)
+    return s;
+  if ((s = stereo_impl(h, right, left, -1, L, label_offset, alpha, tau_color, tau_grad, dR, nullptr, nullptr,
+                       nullptr)) != HGF_OK)
+    return s;
+  return postprocess_impl(h, left, dL, dR, tol, radius, sigma_s, sigma_c, valid_out, disp_out);
 }
 
 hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds, const uint8_t* bg_seeds,

@@ -68,10 +68,18 @@ cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stat
                              int W, int H, int r, int L, float lam0, cudaStream_t st);
 cudaError_t launch_agg_fast(int n, const AggArgs& a, cudaStream_t st);
 // Stereo cost construction (hgf_stereo.cu): dx of the channel mean of a 3-channel view; cost slices of
-// disparities [d0, d0 + Lc) into cost [Lc][H][W].
+// disparities [d0, d0 + Lc) of view `base` against view `other` into cost [Lc][H][W], the match at x - d
+// (dir = +1, the left view's cost) or x + d (dir = -1, the right view's, reading P1).
 cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cudaStream_t st);
-cudaError_t launch_stereo_cost(const float* left, const float* right, const float* gl, const float* gr, float* cost,
-                               int W, int H, int d0, int Lc, float a, float tc, float tg, cudaStream_t st);
+cudaError_t launch_stereo_cost(const float* base, const float* other, const float* gb, const float* go, float* cost,
+                               int W, int H, int d0, int Lc, int dir, float a, float tc, float tg, cudaStream_t st);
+// Post-processing (hgf_stereo.cu, readings P2-P4): consistency flags + row fill, then the weighted median
+// over the inconsistent pixels (radius <= lr_wmf_max_radius()).
+int lr_wmf_max_radius();
+cudaError_t launch_lr_fill(const int* dL, const int* dR, int W, int H, int tol, uint8_t* valid, int* fill,
+                           cudaStream_t st);
+cudaError_t launch_wmf(const int* fill, const uint8_t* valid, const float* img, int m, int W, int H, int radius,
+                       float sigma_s, float sigma_c, int* out, cudaStream_t st);
 // Segmentation costs (hgf_stereo.cu): seed histograms counts [2][m][32], seeds [2] (zeroed by the caller),
 // then the two cost slices [2][H][W].
 cudaError_t launch_seg_hist(const float* img, const uint8_t* fg, const uint8_t* bg, int m, int W, int H, int* counts,

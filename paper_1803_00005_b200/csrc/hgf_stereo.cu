@@ -11,6 +11,7 @@
 // k_stereo_cost: one CTA per 256-pixel row segment; the right-view segment the CTA's disparities touch
 // (256 + Lc - 1 pixels x 4 planes) is staged in SMEM once and reused by every label; one coalesced store
 // per (label, pixel).  HBM traffic: the 4-byte cost write per voxel (re-read by k_coef via TMA).
+#include <climits>
 #include <cstdint>
 
 #include "hgf_common.cuh"
@@ -40,35 +41,38 @@ __global__ void k_stereo_grad(const float* __restrict__ img, float* __restrict__
 
 constexpr int SEG = 256;
 
-__global__ void __launch_bounds__(SEG) k_stereo_cost(const float* __restrict__ left, const float* __restrict__ right,
-                                                     const float* __restrict__ gl, const float* __restrict__ gr,
-                                                     float* __restrict__ cost, int W, int H, int d0, int Lc,
+// dir = +1: the left view's cost (match at x - d in the other view); dir = -1: the right view's cost
+// (reading P1, match at x + d).  `base` is the view whose pixels the slices index, `other` the searched one.
+__global__ void __launch_bounds__(SEG) k_stereo_cost(const float* __restrict__ base, const float* __restrict__ other,
+                                                     const float* __restrict__ gb, const float* __restrict__ go,
+                                                     float* __restrict__ cost, int W, int H, int d0, int Lc, int dir,
                                                      float a, float tc, float tg) {
-  extern __shared__ float rs[];                    // [4][SEG + Lc - 1]: right r, g, b, dx Rbar
+  extern __shared__ float rs[];                    // [4][SEG + Lc - 1]: other view r, g, b, dx of its mean
   const int y = blockIdx.y, x0 = blockIdx.x * SEG, x = x0 + threadIdx.x;
   const long long HW = (long long)W * H, row = (long long)y * W;
   const int span = SEG + Lc - 1;
-  const int xr0 = x0 - (d0 + Lc - 1);             // image column of rs[.][0]
+  // image column of rs[.][0]: the smallest column any (pixel, disparity) of the CTA reads
+  const long long xr0 = dir > 0 ? (long long)x0 - d0 - (Lc - 1) : (long long)x0 + d0;
   for (int i = threadIdx.x; i < span; i += SEG) {
-    const int xr = xr0 + i;
+    const long long xr = xr0 + i;
     const bool in = xr >= 0 && xr < W;
-    rs[i] = in ? __ldg(right + row + xr) : 0.0f;
-    rs[span + i] = in ? __ldg(right + HW + row + xr) : 0.0f;
-    rs[2 * span + i] = in ? __ldg(right + 2 * HW + row + xr) : 0.0f;
-    rs[3 * span + i] = in ? __ldg(gr + row + xr) : 0.0f;
+    rs[i] = in ? __ldg(other + row + xr) : 0.0f;
+    rs[span + i] = in ? __ldg(other + HW + row + xr) : 0.0f;
+    rs[2 * span + i] = in ? __ldg(other + 2 * HW + row + xr) : 0.0f;
+    rs[3 * span + i] = in ? __ldg(go + row + xr) : 0.0f;
   }
   __syncthreads();
   if (x >= W) return;
-  const float lr = __ldg(left + row + x), lg = __ldg(left + HW + row + x), lb = __ldg(left + 2 * HW + row + x);
-  const float lgr = __ldg(gl + row + x);
+  const float lr = __ldg(base + row + x), lg = __ldg(base + HW + row + x), lb = __ldg(base + 2 * HW + row + x);
+  const float lgr = __ldg(gb + row + x);
   const float trunc = a * tc + (1.0f - a) * tg;
   float* out = cost + row + x;
 #pragma unroll 4
   for (int k = 0; k < Lc; ++k) {
-    const int d = d0 + k;
+    const long long xo = (long long)x - (long long)dir * (d0 + k);
     float c = trunc;
-    if (x - d >= 0) {
-      const int i = x - d - xr0;
+    if (xo >= 0 && xo < W) {
+      const int i = (int)(xo - xr0);
       const float col = ((fabsf(lr - rs[i]) + fabsf(lg - rs[span + i])) + fabsf(lb - rs[2 * span + i])) / 3.0f;
       const float grd = fabsf(lgr - rs[3 * span + i]);
       c = a * fminf(col, tc) + (1.0f - a) * fminf(grd, tg);
@@ -86,8 +90,8 @@ cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_stereo_cost(const float* left, const float* right, const float* gl, const float* gr, float* cost,
-                               int W, int H, int d0, int Lc, float a, float tc, float tg, cudaStream_t st) {
+cudaError_t launch_stereo_cost(const float* base, const float* other, const float* gb, const float* go, float* cost,
+                               int W, int H, int d0, int Lc, int dir, float a, float tc, float tg, cudaStream_t st) {
   if (Lc < 1) return cudaSuccess;
   const size_t smem = sizeof(float) * 4 * (size_t)(SEG + Lc - 1);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
@@ -96,7 +100,7 @@ cudaError_t launch_stereo_cost(const float* left, const float* right, const floa
     if (e != cudaSuccess) return e;
   }
   dim3 grid((W + SEG - 1) / SEG, H);
-  k_stereo_cost<<<grid, SEG, smem, st>>>(left, right, gl, gr, cost, W, H, d0, Lc, a, tc, tg);
+  k_stereo_cost<<<grid, SEG, smem, st>>>(base, other, gb, go, cost, W, H, d0, Lc, dir, a, tc, tg);
   return cudaGetLastError();
 }
 
@@ -175,6 +179,184 @@ cudaError_t launch_seg_cost(const float* img, const int* counts, const int* seed
   const long long HW = (long long)W * H;
   const int blocks = (int)((HW + 255) / 256 < 148 * 16 ? (HW + 255) / 256 : 148 * 16);
   k_seg_cost<<<blocks, 256, 0, st>>>(img, counts, seeds, m, W, H, cost);
+  return cudaGetLastError();
+}
+
+}  // namespace hgf
+
+// ----------------------------------------------------------------------------- post-processing (NEXT-3)
+// Readings P2-P4 (P:641 names the step only).
+namespace hgf {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// One warp per row.  Pass 1 (left to right, 32 columns at a time): the consistency flag of every pixel and
+// the index of the nearest consistent pixel at or left of it (inclusive max-scan of "x if consistent else
+// -1" across the warp, carried between chunks), kept in `fill`.  Pass 2 (right to left): the nearest
+// consistent pixel at or right of it (suffix min-scan), then the fill value of P3.
+__global__ void k_lr_fill(const int* __restrict__ dL, const int* __restrict__ dR, int W, int H, int tol,
+                          uint8_t* __restrict__ valid, int* __restrict__ fill) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int y = blockIdx.x * wpb + (threadIdx.x >> 5); y < H; y += gridDim.x * wpb) {
+    const long long row = (long long)y * W;
+    int carry = -1;
+    for (int c0 = 0; c0 < W; c0 += 32) {
+      const int x = c0 + lane;
+      int idx = -1;
+      if (x < W) {
+        const int d = dL[row + x];
+        const long long t = (long long)x - d;
+        bool ok = false;
+        if (t >= 0 && t < W) {
+          const long long diff = (long long)d - dR[row + t];
+          ok = (diff < 0 ? -diff : diff) <= tol;
+        }
+        valid[row + x] = ok ? 1 : 0;
+        idx = ok ? x : -1;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(kFull, idx, off);
+        if (lane >= off) idx = max(idx, v);
+      }
+      idx = max(idx, carry);
+      carry = __shfl_sync(kFull, idx, 31);
+      if (x < W) fill[row + x] = idx;
+    }
+    __syncwarp();
+    carry = W;
+    for (int c0 = ((W - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
+      const int x = c0 + lane;
+      int idx = W;
+      bool ok = true;
+      if (x < W) {
+        ok = valid[row + x] != 0;
+        idx = ok ? x : W;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_down_sync(kFull, idx, off);
+        if (lane + off < 32) idx = min(idx, v);
+      }
+      idx = min(idx, carry);
+      carry = __shfl_sync(kFull, idx, 0);
+      if (x < W && !ok) {
+        const int li = fill[row + x];
+        const bool hl = li >= 0, hr = idx < W;
+        const int vl = hl ? dL[row + li] : 0, vr = hr ? dL[row + idx] : 0;
+        fill[row + x] = (hl && hr) ? min(vl, vr) : (hl ? vl : (hr ? vr : dL[row + x]));
+      } else if (x < W) {
+        fill[row + x] = dL[row + x];
+      }
+    }
+  }
+}
+
+// One warp per 32-pixel run of a row.  Consistent pixels copy the filled map; for each inconsistent pixel
+// (ballot) the whole warp stages the window's values and bilateral weights in SMEM, sums the weights
+// (lane partials in a fixed order, then a shfl_down tree and a broadcast, so every lane holds the same
+// float), and bisects on the disparity: s(d) = sum_{D(q) <= d} w is non-decreasing in d in that fixed
+// order, s(max) equals the total bit for bit, so the smallest d with s(d) >= total / 2 is a window value.
+__device__ __forceinline__ float warp_sum_bcast(float v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+  return __shfl_sync(kFull, v, 0);
+}
+
+__global__ void k_wmf(const int* __restrict__ fill, const uint8_t* __restrict__ valid, const float* __restrict__ img,
+                      int m, int W, int H, int radius, float inv_ss2, float inv_sc2, int* __restrict__ out) {
+  extern __shared__ float wsm[];                   // per warp: [n] weights then [n] values (as int)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int side = 2 * radius + 1, nwin = side * side;
+  float* ws = wsm + (size_t)wib * 2 * nwin;
+  int* vs = reinterpret_cast<int*>(ws + nwin);
+  const long long HW = (long long)W * H;
+  const int runs = (W + 31) / 32;
+  const long long nrun = (long long)runs * H;
+  for (long long rn = (long long)blockIdx.x * wpb + wib; rn < nrun; rn += (long long)gridDim.x * wpb) {
+    const int y = (int)(rn / runs), x = (int)(rn % runs) * 32 + lane;
+    const long long p = (long long)y * W + x;
+    bool todo = false;
+    if (x < W) {
+      todo = valid[p] == 0;
+      if (!todo) out[p] = fill[p];
+    }
+    unsigned pend = __ballot_sync(kFull, todo);
+    while (pend) {
+      const int src = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int px = (int)(rn % runs) * 32 + src;
+      const int y0 = max(0, y - radius), y1 = min(H, y + radius + 1);
+      const int x0 = max(0, px - radius), x1 = min(W, px + radius + 1);
+      const int ww = x1 - x0, n = (y1 - y0) * ww;
+      const long long pc = (long long)y * W + px;
+      float part = 0.0f;
+      int dmin = INT_MAX, dmax = INT_MIN;
+      for (int e = lane; e < n; e += 32) {
+        const int qy = y0 + e / ww, qx = x0 + e % ww;
+        const long long q = (long long)qy * W + qx;
+        float c2 = 0.0f;
+        for (int c = 0; c < m; ++c) {
+          const float dc = __ldg(img + c * HW + q) - __ldg(img + c * HW + pc);
+          c2 = fmaf(dc, dc, c2);
+        }
+        const float dy = (float)(qy - y), dx = (float)(qx - px);
+        const float w = expf(-(dy * dy + dx * dx) * inv_ss2 - c2 * inv_sc2);
+        const int v = fill[q];
+        ws[e] = w;
+        vs[e] = v;
+        part += w;
+        dmin = min(dmin, v);
+        dmax = max(dmax, v);
+      }
+      const float half = 0.5f * warp_sum_bcast(part);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        dmin = min(dmin, __shfl_xor_sync(kFull, dmin, off));
+        dmax = max(dmax, __shfl_xor_sync(kFull, dmax, off));
+      }
+      __syncwarp();
+      long long lo = dmin, hi = dmax;
+      while (lo < hi) {
+        const long long mid = lo + (hi - lo) / 2;
+        float s = 0.0f;
+        for (int e = lane; e < n; e += 32) s += vs[e] <= mid ? ws[e] : 0.0f;
+        if (warp_sum_bcast(s) >= half) hi = mid; else lo = mid + 1;
+      }
+      if (lane == 0) out[pc] = (int)lo;
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace
+
+int lr_wmf_max_radius() { return 15; }
+
+cudaError_t launch_lr_fill(const int* dL, const int* dR, int W, int H, int tol, uint8_t* valid, int* fill,
+                           cudaStream_t st) {
+  const int wpb = 4;
+  const int blocks = (H + wpb - 1) / wpb;
+  k_lr_fill<<<blocks, wpb * 32, 0, st>>>(dL, dR, W, H, tol, valid, fill);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wmf(const int* fill, const uint8_t* valid, const float* img, int m, int W, int H, int radius,
+                       float sigma_s, float sigma_c, int* out, cudaStream_t st) {
+  const int wpb = 8;
+  const int nwin = (2 * radius + 1) * (2 * radius + 1);
+  const size_t smem = sizeof(float) * 2 * (size_t)nwin * wpb;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_wmf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const long long nrun = (long long)((W + 31) / 32) * H;
+  const long long need = (nrun + wpb - 1) / wpb;
+  const int blocks = (int)(need < 148 * 16 ? need : 148 * 16);
+  k_wmf<<<blocks, wpb * 32, smem, st>>>(fill, valid, img, m, W, H, radius, 1.0f / (sigma_s * sigma_s),
+                                       1.0f / (sigma_c * sigma_c), out);
   return cudaGetLastError();
 }
 
