@@ -1,5 +1,7 @@
 // Non-template kernels (K1 guidance, key unpacking) and the n -> template dispatch.
 // The per-n template instantiations live in hgf_inst.cu (compiled once per n with -DHGF_N=n).
+#include <cstdlib>
+
 #include "hgf_common.cuh"
 #include "hgf_launch.h"
 
@@ -64,6 +66,23 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
   // = st2::smem_bytes(n, r): odd-pitch channel tiles, 17-double rows of horizontal sums, vertical sums
   const size_t smem2 = ((size_t)(n + 1) * TS * (TS | 1) * 4 + 15) / 16 * 16 + (size_t)7 * TS * 17 * 8 +
                        (size_t)7 * 16 * 16 * 8 + 16;
+  // k_stats4 (row-marching Gram sums, hgf_stats_v4.cuh) for n <= kStats4MaxN; HGF_STATS2=1 keeps the
+  // tiled k_stats2 (comparison runs)
+  static const bool force2 = std::getenv("HGF_STATS2") != nullptr && std::getenv("HGF_STATS2")[0] == '1';
+  if (!force2 && n <= kStats4MaxN && 64 + 2 * r <= 128 && stats4_smem(n, r) <= 200 * 1024) {
+    switch (n) {
+      case 1: return st4::stats4_impl<1>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 2: return st4::stats4_impl<2>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 3: return st4::stats4_impl<3>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 4: return st4::stats4_impl<4>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 5: return st4::stats4_impl<5>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 6: return st4::stats4_impl<6>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 7: return st4::stats4_impl<7>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 8: return st4::stats4_impl<8>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 9: return st4::stats4_impl<9>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      default: break;
+    }
+  }
   // k_stats3 (Gram planes + warp-per-pixel recursion) where k_stats2 would spill heavily (n >= kStats3MinN)
   // or not fit its channel tiles in shared memory (the O(r) v1 kernel) -- measured on the C5 sweep
   if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= kStats3MinN || (n >= 7 && smem2 > 200 * 1024))) {

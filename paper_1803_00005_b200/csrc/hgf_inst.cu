@@ -70,3 +70,13 @@ template cudaError_t stats2_impl<HGF_N>(const float*, float*, int, int, int, dou
                                         cudaStream_t);
 }  // namespace st2
 }  // namespace hgf
+
+#if HGF_N <= 9
+#include "hgf_stats_v4.cuh"
+namespace hgf {
+namespace st4 {
+template cudaError_t stats4_impl<HGF_N>(const float*, float*, int, int, int, double, int, int, float, int, int,
+                                        cudaStream_t);
+}  // namespace st4
+}  // namespace hgf
+#endif

@@ -1,5 +1,6 @@
 // Internal launcher interface between the C ABI (hgf_api.cu) and the kernels (hgf_kernels.cu).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -31,6 +32,10 @@ cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, 
 // needs the k_stats2 path (else cudaErrorInvalidValue).
 // Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).
 // scratch3: (stats3_scratch_planes(n)) * H * W doubles, or null (k_stats3 is used for n >= kStats3MinN).
+constexpr int kStats4MaxN = 9;      // k_stats4 (row-marching) up to here, when its rows fit SMEM
+inline size_t stats4_smem(int n, int r) {   // = st4::smem_bytes
+  return (size_t)2 * ((n + 1) * (n + 2) / 2 - 1) * (((64 + 2 * r) | 1) + 65) * sizeof(double);
+}
 constexpr int kStats3MinN = 18;     // always k_stats3 from here; below only when k_stats2 does not fit
 inline long long stats3_scratch_planes(int n) { return (long long)(n + 1) * (n + 2) / 2 - 1 + 32; }
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
@@ -133,4 +138,9 @@ template <int NC>
 cudaError_t stats2_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
                         int y0, int y1, cudaStream_t st);
 }  // namespace st2
+namespace st4 {
+template <int NC>
+cudaError_t stats4_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
+                        int y0, int y1, cudaStream_t st);
+}  // namespace st4
 }  // namespace hgf
