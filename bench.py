@@ -2,8 +2,9 @@
 """Benchmark of the HGF hot path (BASELINE.json metric): cost-volume voxels/s aggregated + WTA.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl own|reference]
-Under torchrun (N > 1): one rank per GPU, labels sharded contiguously, keys merged by NCCL
-allreduce-MIN.  Rank 0 prints ONE JSON line.  A "step" = one pass of the whole hot path over one
+Under torchrun (N > 1): one rank per GPU, labels sharded contiguously, statistics replicated (or row-sharded
+with HGF_BENCH_STATS=sharded), keys merged by atomic MIN into the row owners over NVLink (or NCCL
+allreduce-MIN with HGF_BENCH_MERGE=nccl).  Rank 0 prints ONE JSON line.  A "step" = one pass of the whole hot path over one
 synthetic frame: guidance -> float64 statistics -> every label slice filtered -> WTA (-> merge).
 """
 from __future__ import annotations
@@ -186,7 +187,8 @@ def config_json(c, n_gpus):
     return {"workload": workload_name(c), "W": c["W"], "H": c["H"], "labels": c["L"], "n_guide": c["m"],
             "poly_degree": c["d"], "n": c["n"], "radius": c["r"], "lambda": c["lam"],
             "parallelism": (f"labels sharded x{n_gpus} (WTA merged by atomic MIN into the row owners over NVLink, "
-                            "fallback NCCL allreduce-MIN), statistics rows sharded (NCCL all-gather)"
+                            "fallback NCCL allreduce-MIN), statistics " + ("rows sharded (NCCL all-gather)"
+                            if os.environ.get("HGF_BENCH_STATS") == "sharded" else "replicated")
                             if n_gpus > 1 else "single GPU"),
             "l2": "inputs larger than L2 (cost volume > 126 MB); no flush needed"}
 
@@ -326,41 +328,58 @@ def main():
     keys = torch.empty((H, W), dtype=torch.int64, device=dev)
     mincost = torch.empty((H, W), dtype=torch.float32, device=dev)
 
-    # N > 1: statistics row-sharded (each rank its band of rows, NCCL all-gather), slices label-sharded,
-    # WTA merged by the int64 allreduce-MIN of packed keys
-    y0, y1 = shard_range(H, world, rank)
-    row_sharded = False
+    # N > 1: slices label-sharded; the label-independent statistics replicated on every rank by default
+    # (k_stats4 takes ~1.1 ms at C4, less than an NCCL all-gather of the other ranks' 0.93 GB of statistics
+    # rows) or row-sharded + all-gathered (HGF_BENCH_STATS=sharded); WTA merged by the fused peer-memory
+    # merge (default) or the NCCL allreduce-MIN of packed keys (HGF_BENCH_MERGE=nccl) -- DESIGN.md §10
+    stats_mode = os.environ.get("HGF_BENCH_STATS", "replicated")
+    y0, y1 = (0, H) if stats_mode == "replicated" else shard_range(H, world, rank)
+    prepared = False
     if world > 1:
         try:
             h.stats_view()
-            row_sharded = True
+            prepared = True
         except HGFError:
-            row_sharded = False
-    # fused merge (default for N > 1): the aggregation kernel atomicMin's keys into the row owners' buffers
-    # over NVLink (CUDA IPC); HGF_BENCH_MERGE=nccl keeps the allreduce-MIN baseline
-    peer = None
-    if world > 1 and row_sharded and os.environ.get("HGF_BENCH_MERGE", "peer") == "peer":
+            prepared = False
+    row_sharded = prepared and stats_mode != "replicated"
+    # fused merge: the aggregation kernel atomicMin's keys into the row owners' buffers over NVLink (CUDA IPC).
+    # Two owner buffers, used alternately: step s resets the buffer of step s + 1 before its own all-reduce,
+    # so that all-reduce orders every owner's reset before any rank's atomics of step s + 1 (one 4-byte
+    # collective per step, no host sync)
+    peers = None
+    if world > 1 and prepared and os.environ.get("HGF_BENCH_MERGE", "peer") == "peer":
         try:
-            peer = PeerKeys(h)
+            peers = [PeerKeys(h), PeerKeys(h)]
         except Exception as ex:   # no peer mapping on this box: the NCCL merge below
             print(f"[bench] peer merge unavailable ({ex}); using allreduce-MIN", file=sys.stderr)
-            peer = None
+            peers = None
+    peer = peers[0] if peers else None
+    if peers:
+        for pk in peers:
+            pk.reset()
+        torch.cuda.synchronize()
+        dist.barrier()
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     band_labels = labels[: (peer.y1 - peer.y0)] if peer is not None else None
+    nstep = [0]
 
     def step():
         if world == 1:
             h.aggregate_wta(guide, vol, labels)
-        elif peer is not None:
-            peer.reset()
+        elif peers is not None:
+            cur, nxt = peers[nstep[0] % 2], peers[(nstep[0] + 1) % 2]
+            nstep[0] += 1
+            nxt.reset()
             h.prepare_rows(guide, y0, y1)
-            gather_stats_rows(h)          # NCCL all-gather: also orders every owner's reset before any merge
-            h.aggregate_wta_peer(vol, peer.ptrs, world, peer.rows, label_offset=l0)
+            if row_sharded:
+                gather_stats_rows(h)
+            h.aggregate_wta_peer(vol, cur.ptrs, world, cur.rows, label_offset=l0)
             dist.all_reduce(flag)         # every rank's atomics have landed (stream-ordered, no host sync)
-            h.unpack_keys_n(peer.keys[: peer.y1 - peer.y0], band_labels)
-        elif row_sharded:
+            h.unpack_keys_n(cur.keys[: cur.y1 - cur.y0], band_labels)
+        elif prepared:
             h.prepare_rows(guide, y0, y1)
-            gather_stats_rows(h)
+            if row_sharded:
+                gather_stats_rows(h)
             h.aggregate_wta_prepared(vol, label_offset=l0, labels=False, keys=True, out={"keys": keys})
             merge_keys_allreduce(keys)
             h.unpack_keys(keys, labels, mincost)
@@ -486,11 +505,12 @@ def main():
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
             e2e = {"value": W * H * L * args.e2e_steps / float(dt.item()), "unit": UNIT,
                    "h2d_bytes_per_step": 4 * W * H * L + 4 * m * W * H * world, "d2h_bytes_per_step": 4 * W * H,
-                   "api": ("torch H2D copies + HGF.prepare_rows + NCCL all-gather of the statistics rows + "
-                           "HGF.aggregate_wta_peer (keys atomicMin'd into the row owners over NVLink) + "
-                           "HGF.unpack_keys_n" if peer is not None else
-                           "torch H2D copies + HGF.prepare_rows + NCCL all-gather of the statistics rows + "
-                           "HGF.aggregate_wta_prepared + NCCL allreduce-MIN + HGF.unpack_keys" if row_sharded else
+                   "api": ("torch H2D copies + HGF.prepare_rows (" + ("row band + NCCL all-gather of the "
+                           "statistics rows" if row_sharded else "all rows") + ") + " +
+                           ("HGF.aggregate_wta_peer (keys atomicMin'd into the row owners over NVLink) + "
+                            "HGF.unpack_keys_n" if peer is not None else
+                            "HGF.aggregate_wta_prepared + NCCL allreduce-MIN + HGF.unpack_keys")
+                           if prepared else
                            "torch H2D copies + HGF.aggregate_wta_ex + NCCL allreduce-MIN + HGF.unpack_keys")}
 
     cpu = None

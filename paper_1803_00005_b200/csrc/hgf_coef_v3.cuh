@@ -23,6 +23,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include <cuda/ptx>
 
 #include "hgf_common.cuh"
@@ -339,6 +341,8 @@ cudaError_t coef3_r(const void* tm_vol, const void* tm_g, const float* stats, fl
   const int strips = (W + C_TX - 1) / C_TX, batches = (L + Gm::LB - 1) / Gm::LB;
   int BH = 128;
   while (BH > 32 && (long long)strips * ((H + BH - 1) / BH) * batches < 4 * 148) BH /= 2;
+  static const int bh_env = std::getenv("HGF_COEF3_BH") ? std::atoi(std::getenv("HGF_COEF3_BH")) : 0;
+  if (bh_env >= 8) BH = bh_env;                    // tuning runs only
   dim3 grid(strips, (H + BH - 1) / BH, batches);
   k_coef3<NC, R><<<grid, Gm::THREADS, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),
                                                       *reinterpret_cast<const CUtensorMap*>(tm_g), stats, wbuf, wo, W,
