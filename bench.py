@@ -306,7 +306,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1803_00005_b200 import HGF, HGFError, PeerKeys, gather_stats_rows, merge_keys_allreduce, shard_range
+    from paper_1803_00005_b200 import HGF, HGFError, PeerMerge, gather_stats_rows, merge_keys_allreduce, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -342,40 +342,25 @@ def main():
         except HGFError:
             prepared = False
     row_sharded = prepared and stats_mode != "replicated"
-    # fused merge: the aggregation kernel atomicMin's keys into the row owners' buffers over NVLink (CUDA IPC).
-    # Two owner buffers, used alternately: step s resets the buffer of step s + 1 before its own all-reduce,
-    # so that all-reduce orders every owner's reset before any rank's atomics of step s + 1 (one 4-byte
-    # collective per step, no host sync)
-    peers = None
+    # fused merge: the aggregation kernel atomicMin's keys into the row owners' buffers over NVLink (CUDA IPC),
+    # two owner buffers used alternately, one 4-byte collective per step (PeerMerge)
+    peer = None
     if world > 1 and prepared and os.environ.get("HGF_BENCH_MERGE", "peer") == "peer":
         try:
-            peers = [PeerKeys(h), PeerKeys(h)]
+            peer = PeerMerge(h)
         except Exception as ex:   # no peer mapping on this box: the NCCL merge below
             print(f"[bench] peer merge unavailable ({ex}); using allreduce-MIN", file=sys.stderr)
-            peers = None
-    peer = peers[0] if peers else None
-    if peers:
-        for pk in peers:
-            pk.reset()
-        torch.cuda.synchronize()
-        dist.barrier()
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            peer = None
     band_labels = labels[: (peer.y1 - peer.y0)] if peer is not None else None
-    nstep = [0]
 
     def step():
         if world == 1:
             h.aggregate_wta(guide, vol, labels)
-        elif peers is not None:
-            cur, nxt = peers[nstep[0] % 2], peers[(nstep[0] + 1) % 2]
-            nstep[0] += 1
-            nxt.reset()
+        elif peer is not None:
             h.prepare_rows(guide, y0, y1)
             if row_sharded:
                 gather_stats_rows(h)
-            h.aggregate_wta_peer(vol, cur.ptrs, world, cur.rows, label_offset=l0)
-            dist.all_reduce(flag)         # every rank's atomics have landed (stream-ordered, no host sync)
-            h.unpack_keys_n(cur.keys[: cur.y1 - cur.y0], band_labels)
+            peer.aggregate(vol, labels, label_offset=l0)
         elif prepared:
             h.prepare_rows(guide, y0, y1)
             if row_sharded:

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 __all__ = ["HGF", "HGFError", "lib", "lib_path", "MODE_HGF", "MODE_GF", "EXPORTED_SYMBOLS",
-           "merge_keys_allreduce", "shard_range", "gather_stats_rows", "PeerKeys"]
+           "merge_keys_allreduce", "shard_range", "gather_stats_rows", "PeerKeys", "PeerMerge"]
 
 MODE_HGF = 0
 MODE_GF = 1
@@ -488,3 +488,46 @@ class PeerKeys:
             lib().hgf_free(ctypes.c_void_p(self._own))
             self._own = None
 
+
+class PeerMerge:
+    """The fused WTA merge step by step: two PeerKeys owner buffers used alternately.  Step s
+    resets the buffer of step s + 1, runs hgf_aggregate_wta_peer into the buffer of step s, all-reduces a
+    4-byte flag (every rank's atomics of step s have landed; it also orders every owner's reset of the next
+    buffer before any rank's atomics of step s + 1) and unpacks this rank's rows.  One collective per step and
+    no host synchronisation; the statistics must be prepared (``h.prepare_rows`` / ``gather_stats_rows``)."""
+
+    def __init__(self, h, group=None):
+        import torch
+        import torch.distributed as dist
+        self.h, self.group = h, group
+        self.bufs = []
+        try:
+            self.bufs = [PeerKeys(h, group), PeerKeys(h, group)]
+        except Exception:
+            self.close()
+            raise
+        self.world, self.rows = self.bufs[0].world, self.bufs[0].rows
+        self.y0, self.y1 = self.bufs[0].y0, self.bufs[0].y1
+        for b in self.bufs:
+            b.reset()
+        torch.cuda.synchronize(h.device)
+        if self.world > 1:
+            dist.barrier(group=group)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=h.device)
+        self.steps = 0
+
+    def aggregate(self, cost_volume, labels_out, label_offset=0):
+        """One step: labels of this rank's rows [y0, y1) into labels_out[: y1 - y0] (int32, W columns)."""
+        import torch.distributed as dist
+        cur, nxt = self.bufs[self.steps % 2], self.bufs[(self.steps + 1) % 2]
+        self.steps += 1
+        nxt.reset()
+        self.h.aggregate_wta_peer(cost_volume, cur.ptrs, self.world, cur.rows, label_offset=label_offset)
+        if self.world > 1:
+            dist.all_reduce(self.flag, group=self.group)
+        self.h.unpack_keys_n(cur.keys[: self.y1 - self.y0], labels_out[: self.y1 - self.y0])
+
+    def close(self):
+        for b in self.bufs:
+            b.close()
+        self.bufs = []

@@ -399,3 +399,30 @@ def test_peer_merge_equals_allreduce_merge():
     merged = torch.cat(owners)[:H]
     assert torch.equal(merged, ref["keys"])
     h.close()
+
+
+def test_peer_merge_double_buffered_steps():
+    """PeerMerge (the bench's N > 1 step): alternating owner buffers over several steps whose volumes differ,
+    each step's labels equal to the one-call path's (a stale buffer would leak the previous step's minima)."""
+    torch = _torch()
+    from paper_1803_00005_b200 import PeerMerge
+    W, H, L = 152, 61, 20          # the prepared (per-pixel statistics) path needs W % 4 == 0
+    scene = synth.make_stereo_scene(W, H, L, seed=17)
+    gi = torch.from_numpy(scene.left).cuda()
+    base = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    pm = PeerMerge(h)
+    lab = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    h.prepare_rows(gi, 0, H)
+    for s in range(5):
+        # step s: labels permuted and costs raised, so every step has a different WTA map and larger minima
+        perm = torch.roll(torch.arange(L, device="cuda"), s * 3)
+        vol = (base[perm] + 0.01 * s).contiguous()
+        ref = h.aggregate_wta_ex(gi, vol, labels=True)["labels"]
+        h.prepare_rows(gi, 0, H)
+        pm.aggregate(vol, lab)
+        torch.cuda.synchronize()
+        assert torch.equal(lab, ref), s
+    assert pm.steps == 5
+    pm.close()
+    h.close()
