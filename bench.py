@@ -435,6 +435,25 @@ def main():
                 "peak_basis": ("148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts/clock)"
                                if dom != "stats" else "148 SMs x 64 FP64 lanes x 2 x 1965 MHz"),
                 "share_of_step": dom_ms / (ms_max if world == 1 else ms) if ms else None}
+    # the pipe that binds the slice kernels in this design: the SM's L1/shared-memory data pipe, one 128-byte
+    # wavefront per clock per SM (B200_PROFILING.md); ncu's per-launch shared-memory wavefront counts of each
+    # slice kernel (profiles/ncu_smem.json) over its live average launch time
+    smem_pipe = None
+    spath = os.path.join(ROOT, "profiles", "ncu_smem.json")
+    if os.path.exists(spath):
+        try:
+            sj = json.load(open(spath)).get(c["name"], {})
+            wpeak = SM_COUNT * 1965e6 / 1e9
+            smem_pipe = {"unit": "G wavefronts/s (128 B each)", "peak": wpeak,
+                         "basis": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per launch / live launch time; "
+                                  "peak 1 wavefront/clk/SM x 148 SMs x 1965 MHz; TMA writes not counted"}
+            for k in ("coef", "agg"):
+                kms, kcnt = prof[k]
+                if k in sj and kcnt:
+                    ach = sj[k] / (kms / kcnt / 1e3) / 1e9
+                    smem_pipe[k] = {"achieved": ach, "frac": ach / wpeak}
+        except Exception:
+            smem_pipe = None
     stage_ms = {k: v[0] / args.steps for k, v in prof.items()}
     hbm_peak = 6536.0
     try:
@@ -518,7 +537,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (stereo-like v1 generator, seeded; cost volume built in HBM before timing)",
-                "config": config_json(c, world), "roofline": roofline,
+                "config": config_json(c, world), "roofline": roofline, "smem_pipe": smem_pipe,
                 "hbm": {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
                         "alg_bytes_per_step": alg_bytes(W, H, L, m)},
                 "binding_roofline": binding,

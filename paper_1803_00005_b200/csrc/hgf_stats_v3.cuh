@@ -22,7 +22,7 @@ namespace st3 {
 
 constexpr int HX = 128;          // k_gram_h3 / k_gram_v3: pixels per CTA along x
 constexpr int VROWS = 32;        // k_gram_v3: output rows per CTA (vertical sliding restarts per CTA)
-constexpr int PIX = 32;          // k_recur3: pixels per CTA
+constexpr int PIX = 16;          // k_recur3: pixels per CTA
 constexpr int RW = 8;            // k_recur3: warps per CTA
 constexpr int PB = 32;           // product planes per horizontal/vertical batch (bounds the scratch)
 
@@ -79,78 +79,125 @@ __global__ void __launch_bounds__(HX) k_gram_v3(const double* __restrict__ hs, d
   }
 }
 
+// Per-warp dense Gram row pitch (doubles): >= K, even (16-byte aligned rows for the 128-bit broadcasts).
+__host__ __device__ constexpr int gs_pitch(int K) { return (K + 1) / 2 * 2; }
+__host__ __device__ constexpr size_t recur3_smem(int NC) {
+  return sizeof(double) * ((size_t)npairs(NC) * (PIX + 1) + (size_t)RW * (NC + 1) * gs_pitch(NC + 1) + RW * 32) +
+         sizeof(float) * (size_t)(NC * (NC + 1) / 2 + NC) * PIX;
+}
+
 template <int NC>
 __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ gram, float* __restrict__ stats, int W,
                                                     int H, int r, double lam, int mode) {
   constexpr int K = NC + 1, NPAIR = npairs(NC), NP = NC * (NC + 1) / 2, NS = NP + NC;
+  constexpr int GP = PIX + 1;                       // staging pitch: lanes walking pairs spread over the banks
+  constexpr int KP = gs_pitch(K);
   static_assert(K <= 32, "one lane per row of alpha");
   extern __shared__ __align__(16) double sm3[];
-  double* g = sm3;                                  // [NPAIR][PIX]: Gram entries of the CTA's pixels
-  double* ubuf = g + NPAIR * PIX;                   // [RW][32]: u of each warp's current step
+  double* gs_all = sm3;                             // [RW][K][KP]: each warp's pixel, dense (centred) Gram
+  double* g = gs_all + RW * K * KP;                 // [NPAIR][GP]: Gram entries of the CTA's pixels
+  double* ubuf = g + NPAIR * GP;                    // [RW][32]: u of each warp's current step
   float* outs = reinterpret_cast<float*>(ubuf + RW * 32);   // [NS][PIX]: staged outputs
   const long long HW = (long long)H * W;
   const long long pix0 = (long long)blockIdx.x * PIX;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // staging by asynchronous 8-byte copies (cp.async): every load of the CTA is in flight at once instead of
+  // one dependent global load per loop trip (the staging was latency-bound)
   for (int e = tid; e < NPAIR * PIX; e += RW * 32) {
     const int p = e / PIX, k = e % PIX;
     const long long pix = pix0 + k;
-    g[e] = pix < HW ? gram[(long long)p * HW + pix] : 0.0;
+    double* dst = g + p * GP + k;
+    if (pix < HW) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gram + (long long)p * HW + pix)
+                   : "memory");
+    } else {
+      *dst = 0.0;
+    }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   const double inv_lam = 1.0 / lam;
   const int c0 = (mode == 0) ? 0 : 1;
   double* u_s = ubuf + warp * 32;
+  double* gs = gs_all + warp * K * KP;
   for (int k = warp; k < PIX; k += RW) {
     const long long pix = pix0 + k;
     if (pix >= HW) break;
     const int y = (int)(pix / W), x = (int)(pix % W);
     const double N = (double)window_count(y, x, H, W, r);
-    // Gram entry (a, b) of this pixel (centred over channels 1..n in GF mode, §5.1)
-    auto gm = [&](int a, int b) -> double {
-      const int lo = a < b ? a : b, hi = a < b ? b : a;
-      double v = (lo == 0 && hi == 0) ? N : g[pair_index(lo, hi, K) * PIX + k];
-      if (mode != 0 && lo > 0) v -= g[pair_index(0, lo, K) * PIX + k] * g[pair_index(0, hi, K) * PIX + k] / N;
-      return v;
-    };
+    // dense symmetric Gram of this pixel, centred over channels 1..n in GF mode (§5.1), built once
+    for (int e = lane; e < K * K; e += 32) {
+      const int ea = e / K, eb = e % K;
+      const int lo = ea < eb ? ea : eb, hi = ea < eb ? eb : ea;
+      double v = (lo == 0 && hi == 0) ? N : g[pair_index(lo, hi, K) * GP + k];
+      if (mode != 0 && lo > 0) v -= g[pair_index(0, lo, K) * GP + k] * g[pair_index(0, hi, K) * GP + k] / N;
+      gs[ea * KP + eb] = v;
+    }
+    __syncwarp();
     // lane i holds row i of alpha (a[j] = alpha_ij), rows / columns c0 .. kappa filled so far
     double a[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) a[j] = 0.0;
     // F1 (compile-time indices keep a[] in registers)
     if (c0 == 0) {
-      if (lane == 0) a[0] = -inv_lam / (lam + gm(0, 0));
+      if (lane == 0) a[0] = -inv_lam / (lam + gs[0]);
     } else if (lane == 1) {
-      a[1] = -inv_lam / (lam + gm(1, 1));
+      a[1] = -inv_lam / (lam + gs[KP + 1]);
     }
 #pragma unroll
     for (int kap = 1; kap < K; ++kap) {
       if (kap <= c0) continue;
-      // u_i = sum_{m < kap} alpha_im G_m,kap  (lanes c0 .. kap-1)
-      double u = 0.0;
-      if (lane >= c0 && lane < kap) {
+      // column kappa of the Gram (= row kappa), entries 0..kappa: broadcast 128-bit loads
+      double gk[K];
+      const double2* row2 = reinterpret_cast<const double2*>(gs + kap * KP);
 #pragma unroll
-        for (int m = 0; m < kap; ++m)
-          if (m >= c0) u = fma(a[m], gm(m, kap), u);
+      for (int m = 0; m <= kap; m += 2) {
+        const double2 t = row2[m / 2];
+        gk[m] = t.x;
+        if (m + 1 < K) gk[m + 1] = t.y;
       }
-      // quad = sum_i G_kap,i u_i  (warp reduction)
-      double qv = (lane >= c0 && lane < kap) ? gm(kap, lane) * u : 0.0;
+      // u_i = sum_{m < kap} alpha_im G_m,kap  (meaningful in lanes c0 .. kap-1; zero rows elsewhere)
+      double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) qv += __shfl_xor_sync(0xffffffffu, qv, off);
-      const double gam = -1.0 / (1.0 + inv_lam * gm(kap, kap) + qv);               // gamma^kappa
+      for (int m = 0; m < kap; ++m)
+        if (m >= c0) {
+          if (m & 1) u1 = fma(a[m], gk[m], u1);
+          else u0 = fma(a[m], gk[m], u0);
+        }
+      const double u = u0 + u1;
       u_s[lane] = u;
       __syncwarp();
+      double uj[K];
+      const double2* u2 = reinterpret_cast<const double2*>(u_s);
+#pragma unroll
+      for (int j = 0; j < kap; j += 2) {
+        const double2 t = u2[j / 2];
+        uj[j] = t.x;
+        if (j + 1 < K) uj[j + 1] = t.y;
+      }
+      // quad = sum_i G_kap,i u_i, formed by every lane from the broadcast values (no reduction)
+      double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < kap; ++j)
+        if (j >= c0) {
+          if (j & 1) q1 = fma(gk[j], uj[j], q1);
+          else q0 = fma(gk[j], uj[j], q0);
+        }
+      const double gam = -1.0 / (1.0 + inv_lam * gk[kap] + (q0 + q1));             // gamma^kappa
       if (lane >= c0 && lane < kap) {
+        const double gu = gam * u;
 #pragma unroll
         for (int j = 0; j < kap; ++j)
-          if (j >= c0) a[j] = fma(gam * u, u_s[j], a[j]);                            // gamma F + alpha (F2)
-        a[kap] = inv_lam * gam * u;
+          if (j >= c0) a[j] = fma(gu, uj[j], a[j]);                                  // gamma F + alpha (F2)
+        a[kap] = inv_lam * gu;
       } else if (lane == kap) {
 #pragma unroll
         for (int j = 0; j < kap; ++j)
-          if (j >= c0) a[j] = inv_lam * gam * u_s[j];
+          if (j >= c0) a[j] = inv_lam * gam * uj[j];
         a[kap] = inv_lam * inv_lam * gam;
       }
-      __syncwarp();
+      __syncwarp();                                 // u_s is rewritten by the next step
     }
     // outputs: P' = -lambda alpha_{1..n,1..n} (upper triangle, row-major), then nu_k = G_0k / den
     if (lane >= 1 && lane < K) {
@@ -160,8 +207,9 @@ __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ g
       for (int b = 1; b < K; ++b)
         if (b >= ai) outs[(s + (b - ai)) * PIX + k] = (float)(-lam * a[b]);
       const double den = (mode == 0) ? (lam + N) : N;
-      outs[(NP + ai - 1) * PIX + k] = (float)(g[pair_index(0, ai, K) * PIX + k] / den);
+      outs[(NP + ai - 1) * PIX + k] = (float)(g[pair_index(0, ai, K) * GP + k] / den);
     }
+    __syncwarp();                                   // gs is rebuilt for the warp's next pixel
   }
   __syncthreads();
   for (int e = tid; e < NS * PIX; e += RW * 32) {
@@ -175,7 +223,7 @@ __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ g
 template <int NC>
 cudaError_t stats3_impl(const float* G, float* stats, double* scratch, int W, int H, int r, double lam, int mode,
                         cudaStream_t st) {
-  constexpr int NPAIR = npairs(NC), NS = NC * (NC + 1) / 2 + NC;
+  constexpr int NPAIR = npairs(NC);
   const long long HW = (long long)H * W;
   double* gram = scratch;
   double* hs = scratch + (long long)NPAIR * HW;
@@ -189,7 +237,7 @@ cudaError_t stats3_impl(const float* G, float* stats, double* scratch, int W, in
     k_gram_v3<NC><<<gv, HX, 0, st>>>(hs, gram, W, H, r, p0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  const size_t smem = sizeof(double) * ((size_t)NPAIR * PIX + RW * 32) + sizeof(float) * (size_t)NS * PIX;
+  const size_t smem = recur3_smem(NC);
   if ((e = cudaFuncSetAttribute(k_recur3<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
     return e;
   k_recur3<NC><<<(unsigned)((HW + PIX - 1) / PIX), RW * 32, smem, st>>>(gram, stats, W, H, r, lam, mode);
