@@ -85,7 +85,8 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
   }
   // k_stats3 (Gram planes + warp-per-pixel recursion) where k_stats2 would spill heavily (n >= kStats3MinN)
   // or not fit its channel tiles in shared memory (the O(r) v1 kernel) -- measured on the C5 sweep
-  if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= kStats3MinN || (n >= 7 && smem2 > 200 * 1024))) {
+  static const int s3min = std::getenv("HGF_STATS3_MIN_N") ? std::atoi(std::getenv("HGF_STATS3_MIN_N")) : kStats3MinN;
+  if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= s3min || (n >= 7 && smem2 > 200 * 1024))) {
 #define CALL(N) st3::stats3_impl<N>(G, stats, scratch3, W, H, r, lam, mode, st)
     HGF_DISPATCH(n, CALL)
 #undef CALL

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(HX) k_gram_v3(const double* __restrict__ hs, d
 // Per-warp dense Gram row pitch (doubles): >= K, even (16-byte aligned rows for the 128-bit broadcasts).
 __host__ __device__ constexpr int gs_pitch(int K) { return (K + 1) / 2 * 2; }
 __host__ __device__ constexpr size_t recur3_smem(int NC) {
-  return sizeof(double) * ((size_t)npairs(NC) * (PIX + 1) + (size_t)RW * (NC + 1) * gs_pitch(NC + 1) + RW * 32) +
+  return sizeof(double) * (((size_t)npairs(NC) * (PIX + 1) + 1) / 2 * 2 + (size_t)RW * (NC + 1) * gs_pitch(NC + 1) +
+                           RW * 32) +
          sizeof(float) * (size_t)(NC * (NC + 1) / 2 + NC) * PIX;
 }
 
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ g
   extern __shared__ __align__(16) double sm3[];
   double* gs_all = sm3;                             // [RW][K][KP]: each warp's pixel, dense (centred) Gram
   double* g = gs_all + RW * K * KP;                 // [NPAIR][GP]: Gram entries of the CTA's pixels
-  double* ubuf = g + NPAIR * GP;                    // [RW][32]: u of each warp's current step
+  double* ubuf = g + (NPAIR * GP + 1) / 2 * 2;      // [RW][32]: u of each warp's current step (16-B aligned)
   float* outs = reinterpret_cast<float*>(ubuf + RW * 32);   // [NS][PIX]: staged outputs
   const long long HW = (long long)H * W;
   const long long pix0 = (long long)blockIdx.x * PIX;

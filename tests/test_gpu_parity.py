@@ -44,6 +44,9 @@ CASES = [
     ("gray-n1", 40, 33, 1, 1, 3, 4, 0.05, "hgf"),
     ("gray-n3-gf", 40, 33, 1, 3, 3, 3, 0.05, "gf"),
     ("n20", 36, 20, 10, 2, 2, 5, 0.05, "hgf"),
+    # k_stats3 with an odd number of Gram pairs (n = 18: 189; n = 15 at r = 16: 135) -- alignment of its buffers
+    ("n18-gf", 37, 22, 6, 3, 2, 4, 0.05, "gf"),
+    ("n15-r16", 40, 35, 5, 3, 2, 16, 0.05, "hgf"),
     ("r16", 50, 41, 3, 2, 3, 16, 0.05, "hgf"),
     ("r32-small-image", 20, 17, 3, 2, 3, 32, 0.05, "hgf"),
     ("one-row", 67, 1, 3, 2, 3, 3, 0.05, "hgf"),
