@@ -31,33 +31,54 @@ __host__ __device__ constexpr int npairs(int NC) { return (NC + 1) * (NC + 2) / 
 // pair index p of (i, j), 0 <= i <= j <= n, (0,0) excluded: row-major over the upper triangle
 __device__ __forceinline__ int pair_index(int i, int j, int K) { return i * K - i * (i - 1) / 2 + (j - i) - 1; }
 
-// One CTA per (row, 128-pixel segment): all K channel rows staged once, then every pair of the batch.
+// One CTA per (row, 128-pixel segment): all K channel rows staged once (row pitch = 1 mod 32 floats, so
+// lanes reading different channels hit different banks), then items (pair z of the batch, 16-pixel
+// sub-segment s), pairs fastest across the lanes: each slides the 2r+1 window over its 16 pixels in float64
+// (2r+1 products to start, 2 per further pixel: O(1) in r); the sums are staged in SMEM and written out
+// coalesced, one plane row at a time.
+constexpr int HSUB = 16;
+__host__ __device__ inline int gram_h3_span(int r) { return (HX + 2 * r + 31) / 32 * 32 + 1; }
+__host__ __device__ inline size_t gram_h3_smem(int NC, int r) {
+  return ((size_t)(NC + 1) * gram_h3_span(r) * sizeof(float) + 15) / 16 * 16 + (size_t)PB * (HX + 1) * sizeof(double);
+}
 template <int NC>
 __global__ void __launch_bounds__(HX) k_gram_h3(const float* __restrict__ G, double* __restrict__ hs, int W, int H,
                                                  int r, int p0, int pb) {
   constexpr int K = NC + 1;
-  extern __shared__ float row[];                    // [K][HX + 2r]: the channel rows (channel 0 = ones)
-  const int y = blockIdx.y, x0 = blockIdx.x * HX, x = x0 + threadIdx.x;
-  const int span = HX + 2 * r;
+  extern __shared__ __align__(16) unsigned char h3_raw[];
+  float* row = reinterpret_cast<float*>(h3_raw);    // [K][span]: the channel rows (channel 0 = ones)
+  const int span = gram_h3_span(r);
+  double* ob = reinterpret_cast<double*>(h3_raw + ((size_t)K * span * sizeof(float) + 15) / 16 * 16);  // [PB][HX+1]
+  const int y = blockIdx.y, x0 = blockIdx.x * HX;
+  const int wrow = HX + 2 * r;
   const long long HW = (long long)H * W;
-  for (int e = threadIdx.x; e < K * span; e += HX) {
-    const int c = e / span, xx = x0 - r + (e % span);
+  for (int e = threadIdx.x; e < K * wrow; e += HX) {
+    const int c = e / wrow, xx = x0 - r + (e % wrow);
     const bool in = xx >= 0 && xx < W;
-    row[e] = in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)y * W + xx)) : 0.0f;
+    row[c * span + e % wrow] = in ? (c == 0 ? 1.0f : __ldg(G + (c - 1) * HW + (long long)y * W + xx)) : 0.0f;
   }
   __syncthreads();
-  if (x >= W) return;
-  int i = 0, q = p0 + 1;
-  while (q >= K - i) { q -= K - i; ++i; }
-  int j = i + q;
-  for (int z = 0; z < pb; ++z) {
-    const float* ri = row + i * span + threadIdx.x;
-    const float* rj = row + j * span + threadIdx.x;
+  for (int item = threadIdx.x; item < pb * (HX / HSUB); item += HX) {
+    const int z = item % pb, sub = item / pb;
+    int i = 0, q = p0 + z + 1;
+    while (q >= K - i) { q -= K - i; ++i; }
+    const int j = i + q;
+    const float* ri = row + i * span + sub * HSUB;
+    const float* rj = row + j * span + sub * HSUB;
+    double* o = ob + z * (HX + 1) + sub * HSUB;
     double acc = 0.0;
-    for (int dx = 0; dx <= 2 * r; ++dx) acc += (double)ri[dx] * (double)rj[dx];
-    hs[(long long)z * HW + (long long)y * W + x] = acc;
-    if (++j == K) { ++i; j = i; }
+    for (int dx = 0; dx <= 2 * r; ++dx) acc = fma((double)ri[dx], (double)rj[dx], acc);
+    o[0] = acc;
+#pragma unroll
+    for (int t = 1; t < HSUB; ++t) {
+      acc = fma((double)ri[t + 2 * r], (double)rj[t + 2 * r], fma(-(double)ri[t - 1], (double)rj[t - 1], acc));
+      o[t] = acc;
+    }
   }
+  __syncthreads();
+  const int x = x0 + threadIdx.x;
+  if (x >= W) return;
+  for (int z = 0; z < pb; ++z) hs[(long long)z * HW + (long long)y * W + x] = ob[z * (HX + 1) + threadIdx.x];
 }
 
 template <int NC>   // (templated only so that every per-n translation unit owns its instance)
@@ -228,11 +249,13 @@ cudaError_t stats3_impl(const float* G, float* stats, double* scratch, int W, in
   const long long HW = (long long)H * W;
   double* gram = scratch;
   double* hs = scratch + (long long)NPAIR * HW;
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_gram_h3<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)gram_h3_smem(NC, r));
+  if (e != cudaSuccess) return e;
   for (int p0 = 0; p0 < NPAIR; p0 += PB) {
     const int pb = NPAIR - p0 < PB ? NPAIR - p0 : PB;
     dim3 gh((W + HX - 1) / HX, H);
-    k_gram_h3<NC><<<gh, HX, sizeof(float) * (NC + 1) * (HX + 2 * r), st>>>(G, hs, W, H, r, p0, pb);
+    k_gram_h3<NC><<<gh, HX, gram_h3_smem(NC, r), st>>>(G, hs, W, H, r, p0, pb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     dim3 gv((W + HX - 1) / HX, (H + VROWS - 1) / VROWS, pb);
     k_gram_v3<NC><<<gv, HX, 0, st>>>(hs, gram, W, H, r, p0);
