@@ -108,6 +108,100 @@ __host__ __device__ constexpr size_t recur3_smem(int NC) {
          sizeof(float) * (size_t)(NC * (NC + 1) / 2 + NC) * PIX;
 }
 
+// One pixel's recursion on one warp (C0 = 0: HGF mode, all n+1 coefficients penalised; C0 = 1: GF mode,
+// centred Gram, alpha from index 1 on -- compile-time, so the unrolled steps carry no runtime mode tests).
+template <int NC, int C0>
+__device__ __forceinline__ void recur3_pixel(const double* __restrict__ g, double* __restrict__ gs,
+                                             double* __restrict__ u_s, float* __restrict__ outs, int k, int lane,
+                                             double N, double lam) {
+  constexpr int K = NC + 1, NP = NC * (NC + 1) / 2;
+  constexpr int GP = PIX + 1, KP = gs_pitch(K);
+  const double inv_lam = 1.0 / lam;
+  // dense symmetric Gram of this pixel, centred over channels 1..n in GF mode (§5.1), built once
+  for (int e = lane; e < K * K; e += 32) {
+    const int ea = e / K, eb = e % K;
+    const int lo = ea < eb ? ea : eb, hi = ea < eb ? eb : ea;
+    double v = (lo == 0 && hi == 0) ? N : g[pair_index(lo, hi, K) * GP + k];
+    if (C0 != 0 && lo > 0) v -= g[pair_index(0, lo, K) * GP + k] * g[pair_index(0, hi, K) * GP + k] / N;
+    gs[ea * KP + eb] = v;
+  }
+  __syncwarp();
+  // lane i holds row i of alpha (a[j] = alpha_ij), rows / columns c0 .. kappa filled so far
+  double a[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) a[j] = 0.0;
+  // F1 (compile-time indices keep a[] in registers)
+  if (C0 == 0) {
+    if (lane == 0) a[0] = -inv_lam / (lam + gs[0]);
+  } else if (lane == 1) {
+    a[1] = -inv_lam / (lam + gs[KP + 1]);
+  }
+#pragma unroll
+  for (int kap = 1; kap < K; ++kap) {
+    if (kap <= C0) continue;
+    // column kappa of the Gram (= row kappa), entries 0..kappa: broadcast 128-bit loads
+    double gk[K];
+    const double2* row2 = reinterpret_cast<const double2*>(gs + kap * KP);
+#pragma unroll
+    for (int m = 0; m <= kap; m += 2) {
+      const double2 t = row2[m / 2];
+      gk[m] = t.x;
+      if (m + 1 < K) gk[m + 1] = t.y;
+    }
+    // u_i = sum_{m < kap} alpha_im G_m,kap  (meaningful in lanes c0 .. kap-1; zero rows elsewhere)
+    double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < kap; ++m)
+      if (m >= C0) {
+        if (m & 1) u1 = fma(a[m], gk[m], u1);
+        else u0 = fma(a[m], gk[m], u0);
+      }
+    const double u = u0 + u1;
+    u_s[lane] = u;
+    __syncwarp();
+    double uj[K];
+    const double2* u2 = reinterpret_cast<const double2*>(u_s);
+#pragma unroll
+    for (int j = 0; j < kap; j += 2) {
+      const double2 t = u2[j / 2];
+      uj[j] = t.x;
+      if (j + 1 < K) uj[j + 1] = t.y;
+    }
+    // quad = sum_i G_kap,i u_i, formed by every lane from the broadcast values (no reduction)
+    double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < kap; ++j)
+      if (j >= C0) {
+        if (j & 1) q1 = fma(gk[j], uj[j], q1);
+        else q0 = fma(gk[j], uj[j], q0);
+      }
+    const double gam = -1.0 / (1.0 + inv_lam * gk[kap] + (q0 + q1));             // gamma^kappa
+    if (lane >= C0 && lane < kap) {
+      const double gu = gam * u;
+#pragma unroll
+      for (int j = 0; j < kap; ++j)
+        if (j >= C0) a[j] = fma(gu, uj[j], a[j]);                                  // gamma F + alpha (F2)
+      a[kap] = inv_lam * gu;
+    } else if (lane == kap) {
+#pragma unroll
+      for (int j = 0; j < kap; ++j)
+        if (j >= C0) a[j] = inv_lam * gam * uj[j];
+      a[kap] = inv_lam * inv_lam * gam;
+    }
+    __syncwarp();                                 // u_s is rewritten by the next step
+  }
+  // outputs: P' = -lambda alpha_{1..n,1..n} (upper triangle, row-major), then nu_k = G_0k / den
+  if (lane >= 1 && lane < K) {
+    const int ai = lane;
+    int s = (ai - 1) * NC - (ai - 1) * (ai - 2) / 2;     // first upper-triangle slot of row ai
+#pragma unroll
+    for (int b = 1; b < K; ++b)
+      if (b >= ai) outs[(s + (b - ai)) * PIX + k] = (float)(-lam * a[b]);
+    const double den = (C0 == 0) ? (lam + N) : N;
+    outs[(NP + ai - 1) * PIX + k] = (float)(g[pair_index(0, ai, K) * GP + k] / den);
+  }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ gram, float* __restrict__ stats, int W,
                                                     int H, int r, double lam, int mode) {
@@ -139,8 +233,6 @@ __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ g
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  const double inv_lam = 1.0 / lam;
-  const int c0 = (mode == 0) ? 0 : 1;
   double* u_s = ubuf + warp * 32;
   double* gs = gs_all + warp * K * KP;
   for (int k = warp; k < PIX; k += RW) {
@@ -148,89 +240,8 @@ __global__ void __launch_bounds__(RW * 32) k_recur3(const double* __restrict__ g
     if (pix >= HW) break;
     const int y = (int)(pix / W), x = (int)(pix % W);
     const double N = (double)window_count(y, x, H, W, r);
-    // dense symmetric Gram of this pixel, centred over channels 1..n in GF mode (§5.1), built once
-    for (int e = lane; e < K * K; e += 32) {
-      const int ea = e / K, eb = e % K;
-      const int lo = ea < eb ? ea : eb, hi = ea < eb ? eb : ea;
-      double v = (lo == 0 && hi == 0) ? N : g[pair_index(lo, hi, K) * GP + k];
-      if (mode != 0 && lo > 0) v -= g[pair_index(0, lo, K) * GP + k] * g[pair_index(0, hi, K) * GP + k] / N;
-      gs[ea * KP + eb] = v;
-    }
-    __syncwarp();
-    // lane i holds row i of alpha (a[j] = alpha_ij), rows / columns c0 .. kappa filled so far
-    double a[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) a[j] = 0.0;
-    // F1 (compile-time indices keep a[] in registers)
-    if (c0 == 0) {
-      if (lane == 0) a[0] = -inv_lam / (lam + gs[0]);
-    } else if (lane == 1) {
-      a[1] = -inv_lam / (lam + gs[KP + 1]);
-    }
-#pragma unroll
-    for (int kap = 1; kap < K; ++kap) {
-      if (kap <= c0) continue;
-      // column kappa of the Gram (= row kappa), entries 0..kappa: broadcast 128-bit loads
-      double gk[K];
-      const double2* row2 = reinterpret_cast<const double2*>(gs + kap * KP);
-#pragma unroll
-      for (int m = 0; m <= kap; m += 2) {
-        const double2 t = row2[m / 2];
-        gk[m] = t.x;
-        if (m + 1 < K) gk[m + 1] = t.y;
-      }
-      // u_i = sum_{m < kap} alpha_im G_m,kap  (meaningful in lanes c0 .. kap-1; zero rows elsewhere)
-      double u0 = 0.0, u1 = 0.0;
-#pragma unroll
-      for (int m = 0; m < kap; ++m)
-        if (m >= c0) {
-          if (m & 1) u1 = fma(a[m], gk[m], u1);
-          else u0 = fma(a[m], gk[m], u0);
-        }
-      const double u = u0 + u1;
-      u_s[lane] = u;
-      __syncwarp();
-      double uj[K];
-      const double2* u2 = reinterpret_cast<const double2*>(u_s);
-#pragma unroll
-      for (int j = 0; j < kap; j += 2) {
-        const double2 t = u2[j / 2];
-        uj[j] = t.x;
-        if (j + 1 < K) uj[j + 1] = t.y;
-      }
-      // quad = sum_i G_kap,i u_i, formed by every lane from the broadcast values (no reduction)
-      double q0 = 0.0, q1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < kap; ++j)
-        if (j >= c0) {
-          if (j & 1) q1 = fma(gk[j], uj[j], q1);
-          else q0 = fma(gk[j], uj[j], q0);
-        }
-      const double gam = -1.0 / (1.0 + inv_lam * gk[kap] + (q0 + q1));             // gamma^kappa
-      if (lane >= c0 && lane < kap) {
-        const double gu = gam * u;
-#pragma unroll
-        for (int j = 0; j < kap; ++j)
-          if (j >= c0) a[j] = fma(gu, uj[j], a[j]);                                  // gamma F + alpha (F2)
-        a[kap] = inv_lam * gu;
-      } else if (lane == kap) {
-#pragma unroll
-        for (int j = 0; j < kap; ++j)
-          if (j >= c0) a[j] = inv_lam * gam * uj[j];
-        a[kap] = inv_lam * inv_lam * gam;
-      }
-      __syncwarp();                                 // u_s is rewritten by the next step
-    }
-    // outputs: P' = -lambda alpha_{1..n,1..n} (upper triangle, row-major), then nu_k = G_0k / den
-    if (lane >= 1 && lane < K) {
-      const int ai = lane;
-      int s = (ai - 1) * NC - (ai - 1) * (ai - 2) / 2;     // first upper-triangle slot of row ai
-#pragma unroll
-      for (int b = 1; b < K; ++b)
-        if (b >= ai) outs[(s + (b - ai)) * PIX + k] = (float)(-lam * a[b]);
-      const double den = (mode == 0) ? (lam + N) : N;
-      outs[(NP + ai - 1) * PIX + k] = (float)(g[pair_index(0, ai, K) * GP + k] / den);
-    }
+    if (mode == 0) recur3_pixel<NC, 0>(g, gs, u_s, outs, k, lane, N, lam);
+    else recur3_pixel<NC, 1>(g, gs, u_s, outs, k, lane, N, lam);
     __syncwarp();                                   // gs is rebuilt for the warp's next pixel
   }
   __syncthreads();
