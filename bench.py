@@ -545,6 +545,8 @@ def main():
                 "segmentation": segmentation,
                 "gpu_launches": int(lt.item()), "clocks": clk}
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     h.close()
     if world > 1:
         dist.destroy_process_group()

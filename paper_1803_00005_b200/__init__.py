@@ -528,6 +528,14 @@ class PeerMerge:
         self.h.unpack_keys_n(cur.keys[: self.y1 - self.y0], labels_out[: self.y1 - self.y0])
 
     def close(self):
+        """Unmap the peers' buffers, wait for every rank to have done so, then free this rank's own."""
+        import torch.distributed as dist
+        for b in self.bufs:
+            for q in b._opened:
+                lib().hgf_ipc_close(ctypes.c_void_p(q))
+            b._opened = []
+        if self.bufs and getattr(self, "world", 1) > 1 and dist.is_initialized():
+            dist.barrier(group=self.group)
         for b in self.bufs:
             b.close()
         self.bufs = []
