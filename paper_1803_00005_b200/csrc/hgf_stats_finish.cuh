@@ -12,10 +12,11 @@ namespace hgf {
 
 // g: the NPAIR = (n+1)(n+2)/2 - 1 Gram sums of pixel p, pairs (a, b), a <= b, enumerated row-major over the
 // upper triangle with (0, 0) skipped.  Writes the record (aos) or the planar statistics of pixel p.
-template <int NC>
-__device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 2) / 2 - 1], double N, double lam,
-                                             int mode, int aos, float lam0f, float* __restrict__ stats, long long p,
-                                             long long HW) {
+template <int NC, int MODE>
+__device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC + 2) / 2 - 1], double N, double lam,
+                                               int aos, float lam0f, float* __restrict__ stats, long long p,
+                                               long long HW) {
+  constexpr int mode = MODE;   // compile-time: no runtime mode tests in the unrolled recursion
   constexpr int K = NC + 1;
   double Gm[K][K];
 #pragma unroll
@@ -28,12 +29,16 @@ __device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 
       Gm[b][a] = v;
     }
   const double inv_lam = 1.0 / lam;
-  const int c0 = (mode == 0) ? 0 : 1;
+  constexpr int c0 = (mode == 0) ? 0 : 1;
   if (mode != 0) {
+    const double invN = 1.0 / N;
 #pragma unroll
     for (int a = 1; a < K; ++a)
 #pragma unroll
-      for (int b = 1; b < K; ++b) Gm[a][b] = Gm[a][b] - Gm[0][a] * Gm[0][b] / N;   // centred Gram (§5.1)
+      for (int b = a; b < K; ++b) {
+        Gm[a][b] = Gm[a][b] - Gm[0][a] * Gm[0][b] * invN;                          // centred Gram (§5.1)
+        Gm[b][a] = Gm[a][b];
+      }
   }
   double al[K][K];
 #pragma unroll
@@ -69,7 +74,7 @@ __device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 
     }
     al[k][k] = inv_lam * inv_lam * gam;
   }
-  const double den = (mode == 0) ? (lam + N) : N;
+  const double inv_den = 1.0 / ((mode == 0) ? (lam + N) : N);   // one division, then products
   if (aos) {
     constexpr int REC = stats_aos_floats(NC);
     float rec[REC];
@@ -79,7 +84,7 @@ __device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 
 #pragma unroll
       for (int b = a; b < K; ++b) rec[s++] = (float)(-lam * al[a][b]);
 #pragma unroll
-    for (int a = 1; a < K; ++a) rec[s++] = (float)(Gm[0][a] / den);
+    for (int a = 1; a < K; ++a) rec[s++] = (float)(Gm[0][a] * inv_den);
     rec[s++] = 1.0f / (lam0f + (float)N);
 #pragma unroll
     for (; s < REC; ++s) rec[s] = 0.0f;
@@ -94,7 +99,15 @@ __device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 
 #pragma unroll
     for (int b = a; b < K; ++b) stats[(long long)(s++) * HW + p] = (float)(-lam * al[a][b]);
 #pragma unroll
-  for (int a = 1; a < K; ++a) stats[(long long)(s++) * HW + p] = (float)(Gm[0][a] / den);
+  for (int a = 1; a < K; ++a) stats[(long long)(s++) * HW + p] = (float)(Gm[0][a] * inv_den);
+}
+
+template <int NC>
+__device__ __forceinline__ void stats_finish(const double (&g)[(NC + 1) * (NC + 2) / 2 - 1], double N, double lam,
+                                             int mode, int aos, float lam0f, float* __restrict__ stats, long long p,
+                                             long long HW) {
+  if (mode == 0) stats_finish_m<NC, 0>(g, N, lam, aos, lam0f, stats, p, HW);
+  else stats_finish_m<NC, 1>(g, N, lam, aos, lam0f, stats, p, HW);
 }
 
 }  // namespace hgf
