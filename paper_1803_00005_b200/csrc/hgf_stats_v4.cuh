@@ -22,6 +22,10 @@
 #include "hgf_launch.h"
 #include "hgf_stats_finish.cuh"
 
+#ifndef HGF_ST4_EXP
+#define HGF_ST4_EXP 0   // timing experiments only: 1 = no R phase, 2 = no H phase, 3 = neither (wrong results)
+#endif
+
 namespace hgf {
 namespace st4 {
 
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
     if (yb + RB <= Z0) continue;                 // rows before the requested range: V only (same thread)
     __syncthreads();
     // ---- H phase: sliding 2r+1-column window sums per (rb, segment, pair)
-    for (int item = tid; item < RB * NSEG * NPAIR; item += THREADS) {
+    for (int item = tid; item < ((HGF_ST4_EXP & 2) ? 0 : RB * NSEG * NPAIR); item += THREADS) {
       const int q = item % NPAIR, sg = (item / NPAIR) % NSEG, rb = item / (NPAIR * NSEG);
       const double* v = vs + (rb * NPAIR + q) * VXP + sg * HSEG;
       double* o = hs + (rb * NPAIR + q) * TXP + sg * HSEG;
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
     {
       const int rb = tid / TX, x = tid % TX;
       const int gy = yb + rb, gx = x0 + x;
-      if (gy >= Z0 && gy < Z1 && gx < W) {
+      if (!(HGF_ST4_EXP & 1) && gy >= Z0 && gy < Z1 && gx < W) {
         double g[NPAIR];
         const double* src = hs + rb * NPAIR * TXP + x;
 #pragma unroll
