@@ -47,6 +47,9 @@ CASES = [
     # k_stats3 with an odd number of Gram pairs (n = 18: 189; n = 15 at r = 16: 135) -- alignment of its buffers
     ("n18-gf", 37, 22, 6, 3, 2, 4, 0.05, "gf"),
     ("n15-r16", 40, 35, 5, 3, 2, 16, 0.05, "hgf"),
+    # k_stats3 at the maximum radius (k_stats2's tiles do not fit): odd pair count (n = 11: 77), GF n = 20
+    ("n11-r32", 40, 30, 11, 1, 2, 32, 0.05, "hgf"),
+    ("n20-r32-gf", 33, 35, 10, 2, 2, 32, 0.05, "gf"),
     ("r16", 50, 41, 3, 2, 3, 16, 0.05, "hgf"),
     ("r32-small-image", 20, 17, 3, 2, 3, 32, 0.05, "hgf"),
     ("one-row", 67, 1, 3, 2, 3, 3, 0.05, "hgf"),
