@@ -16,7 +16,8 @@ __all__ = ["HGF", "HGFError", "lib", "lib_path", "MODE_HGF", "MODE_GF", "EXPORTE
 MODE_HGF = 0
 MODE_GF = 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libhgf.so")
+# HGF_LIB_PATH: an alternate build of the same library (A/B timing builds only; still the CUDA path)
+lib_path = os.environ.get("HGF_LIB_PATH") or os.path.join(_HERE, "libhgf.so")
 
 # Every entry point declared in include/hgf.h (tests check the .so exports all of them).
 EXPORTED_SYMBOLS = (
