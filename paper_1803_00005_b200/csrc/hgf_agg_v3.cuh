@@ -19,7 +19,7 @@
 //     (planar: 8 lanes of a quarter-warp read 8 different rows; the row pitch BX has BX/4 odd).
 //
 // IL = true reads the label-interleaved coefficient layout written by k_coef3 (WLayout::il): a rank-5
-// tensor map (16 px, 32 labels, x groups, y, planes) with box (16, 1, BX/16, BY, planes) lands the same
+// tensor map (G px, 32 labels, x groups, y, planes) with box (G, 1, BX/G, BY, planes), G = kWGroupPx, lands the same
 // [k][y][x] tile (BX a multiple of 32) with the 64-byte TMA swizzle: the 16-byte chunk c of 64-byte row
 // R sits at chunk c ^ ((R >> 1) & 3), i.e. float index f -> f ^ ((f >> 3) & 12) from a 1 KB aligned
 // buffer.  The swizzle keeps both passes conflict-free without a padded pitch; owners then map a
@@ -60,10 +60,14 @@ struct AggGeom {
   static_assert(K >= 2, "two plane groups");
 };
 
-// SMEM float index of logical tile element f under the 64-byte TMA swizzle (identity without it).
+// 8-pixel groups (HGF_WG8) give 32-byte TMA inner runs, which take the 32-byte swizzle instead (the 64-byte
+// one needs 64-byte rows and faults on 32-byte ones: tools/tma_swz8.cu, profiles/r01_tma_swz8.txt): the
+// 16-byte chunk c of 32-byte row R sits at c ^ ((R >> 2) & 1), i.e. f -> f ^ ((f >> 3) & 4).
+constexpr bool kSw32 = kWGroupPx == 8;
+// SMEM float index of logical tile element f under the TMA swizzle (identity without it).
 template <bool IL>
 __device__ __forceinline__ int swz(int f) {
-  return IL ? (f ^ ((f >> 3) & 12)) : f;
+  return IL ? (kSw32 ? (f ^ ((f >> 3) & 4)) : (f ^ ((f >> 3) & 12))) : f;
 }
 
 // mbarrier / TMA wrappers over libcu++'s cuda::ptx (PTX ISA 8.0+, sm_90+).
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
   uint64_t* bar = reinterpret_cast<uint64_t*>(buf + Gm::FLOATS);
   const int tid = threadIdx.x;
   // Tiles start at x0 = 64*bx - XSHIFT so that the TMA x coordinate x0 - R is a multiple of 4 (16 bytes;
-  // IL: of one 16-pixel group): TMA traps on x offsets that are not 16-byte aligned (tools/tma_test2.cu);
+  // IL: of one kWGroupPx-pixel group): TMA traps on x offsets that are not 16-byte aligned (tools/tma_test2.cu);
   // negative coordinates and the out-of-bounds zero fill are fine, and implement the clipped windows.
   constexpr int XALIGN = IL ? kWGroupPx : 4;
   constexpr int XSHIFT = (XALIGN - R % XALIGN) % XALIGN;
@@ -151,9 +155,12 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
   // owner role: row oy, pixels x0 + 8*seg + [0, 8)
   const bool is_owner = tid < NOWN;
   const int wq = tid >> 5, ln = tid & 31;
-  // planar: a quarter-warp = 8 rows of one segment (odd BX/4 pitch); IL: 4 rows x segments s, s + 2
-  const int oy = IL ? (ln & 3) + 4 * wq : (ln & 7) + 8 * (wq % 3);
-  const int seg = IL ? ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1) : (ln >> 3) + 4 * (wq / 3);
+  // planar: a quarter-warp = 8 rows of one segment (odd BX/4 pitch); IL: 4 rows x segments s, s + 2;
+  // IL with the 32-byte swizzle: one row x all 8 segments (segments s and s + 4 share a chunk index and are
+  // told apart by the swizzle bit; tools/swizzle_banks.py checks R = 1..32)
+  const int oy = IL ? (kSw32 ? (ln >> 3) + 4 * wq : (ln & 3) + 4 * wq) : (ln & 7) + 8 * (wq % 3);
+  const int seg = IL ? (kSw32 ? (ln & 7) : ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1))
+                     : (ln >> 3) + 4 * (wq / 3);
   const int gy = y0 + oy;
   float g[NC > 0 ? NC : 1][KX];
   float invN[KX], best[KX];
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
   }
 
   // owner row-segment offsets of plane 0 (swizzled); PLANE/32 is even, so other planes differ by bit 3 at most
-  static_assert(!IL || ((PLANE / 32) & 1) == 0, "plane swizzle phase");
+  static_assert(!IL || kSw32 || ((PLANE / 32) & 1) == 0, "plane swizzle phase");
   int ofs[NV4];
 #pragma unroll
   for (int q = 0; q < NV4; ++q) ofs[q] = swz<IL>(oy * BX + seg * KX + 4 * q);
@@ -196,7 +203,10 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
         // (BX is a multiple of 32 floats, so adding y*BX never carries into the swizzled bits)
         int fb[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fb[j] = IL ? (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 3) << 2)) : f0;
+        for (int j = 0; j < 4; ++j)
+          fb[j] = IL ? (kSw32 ? (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 1) << 2))
+                              : (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 3) << 2)))
+                     : f0;
         float col[BY];
 #pragma unroll
         for (int y = 0; y < BY; ++y) col[y] = lb[fb[y & 3] + y * BX];
@@ -217,7 +227,10 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
         for (int k = (h == 0 ? 0 : KA); k < (h == 0 ? KA : K); ++k) {
           // plane kk of the group: swizzle mask of plane 0 flipped in bit 3 when kk * PLANE/32 = 2 mod 4
           const int kk = k - k0;
-          const int flip = (IL && ((kk * ((PLANE / 32) & 3)) & 3) == 2) ? 8 : 0;
+          // (32-byte swizzle: flipped in bit 2 when kk * PLANE/32 is odd)
+          const int flip = !IL ? 0
+                           : kSw32 ? (((kk * (PLANE / 32)) & 1) ? 4 : 0)
+                                   : ((((kk * ((PLANE / 32) & 3)) & 3) == 2) ? 8 : 0);
           float f[4 * NV4];
 #pragma unroll
           for (int q = 0; q < NV4; ++q) {

@@ -246,8 +246,8 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
     const cuuint32_t planes = (cuuint32_t)(grp == 0 ? KA : K - KA);
     CUresult r;
     if (h->wlay.il) {
-      // rank 5 over the label-interleaved layout: (16 px, 32 labels, x groups, y, label-batch planes); one
-      // box = one label's planes of a BX x BY tile, 64-byte inner runs with the matching 64-byte swizzle
+      // rank 5 over the label-interleaved layout: (G px, 32 labels, x groups, y, label-batch planes); one
+      // box = one label's planes of a BX x BY tile, 4G-byte inner runs, 64-byte swizzle (k_agg3's swz)
       const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
       const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
                                   (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * K};
@@ -255,7 +255,9 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
       const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, planes};
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
       r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 hgf::kWGroupPx == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),

@@ -39,7 +39,7 @@ namespace v3 {
 constexpr int C_TX = 64;                    // owned columns per strip
 constexpr int C_LG = 8;                     // labels per V thread
 constexpr int C_HSEG = 16;                  // pixels per H thread (two store groups of 8)
-static_assert(C_HSEG == kWGroupPx, "an H segment is one group of the interleaved layout");
+static_assert(C_HSEG % kWGroupPx == 0 && kWGroupPx % 8 == 0, "an H segment is whole groups of the interleaved layout");
 constexpr int C_NSEG = C_TX / C_HSEG;       // segments per strip
 constexpr int C_RMAX = 9;
 constexpr int C_BXP = 88;                   // TMA box width: >= TX + 2*RMAX + 3 (x start rounded down to 16 B)
@@ -297,13 +297,13 @@ __global__ void __launch_bounds__(CoefGeom<NC>::THREADS, 1)
         wv[0][ii] = w0;
       }
       if (wo.il) {
-        // label-interleaved layout: this lane's 16-pixel segment is one group; 32-byte stores, and the 16
-        // labels of the half-warp cover one contiguous 1 KB run (see WLayout)
-        const int grp = (x0 + xs) / kWGroupPx;
+        // label-interleaved layout (see WLayout): 32-byte stores of 8 pixels; G = 16: the 16 labels of a
+        // half-warp cover one contiguous 1 KB run; G = 8: the 32 labels of a warp do (whole lines)
+        const int grp = (x0 + xs + q8) / kWGroupPx;
         if (lok && grp < wo.xg) {
           float* wg = wbuf + (((long long)(l / kWGroupLabels) * K * H + y) * wo.xg + grp) *
                                  (kWGroupPx * kWGroupLabels) +
-                      (l % kWGroupLabels) * kWGroupPx + q8;
+                      (l % kWGroupLabels) * kWGroupPx + q8 % kWGroupPx;
           const long long kstride = (long long)H * wo.xg * (kWGroupPx * kWGroupLabels);
 #pragma unroll
           for (int k = 0; k < K; ++k) st_global_v8(wg + k * kstride, wv[k]);

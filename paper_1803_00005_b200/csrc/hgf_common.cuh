@@ -34,11 +34,16 @@ __device__ __forceinline__ int64_t pack_key_signed(float cost, int32_t label) {
 // Layout of the per-slice coefficient buffer.
 // Planar (il == 0): element (label l, plane k, y, x) of a chunk lives at
 //   origin + (l*(n+1) + k)*plane + y*pitch + x.
-// Label-interleaved (il == 1, k_coef3 -> k_agg3): 32 labels share each 16-pixel group,
-//   ((((l/32)*(n+1) + k)*H + y)*xg + x/16)*512 + (l%32)*16 + x%16,
-// so the 16 labels of a k_coef3 half-warp store one contiguous 1 KB run per instruction, and k_agg3's TMA
-// still reads 64-byte runs of one label (16 pixels) per request.
-constexpr int kWGroupPx = 16, kWGroupLabels = 32;
+// Label-interleaved (il == 1, k_coef3 -> k_agg3): 32 labels share each G-pixel group (G = kWGroupPx),
+//   ((((l/32)*(n+1) + k)*H + y)*xg + x/G)*(32*G) + (l%32)*G + x%G.
+// G = 16 (default): the 16 labels of a k_coef3 half-warp store one contiguous 1 KB run per instruction
+// (each 128-byte line half-written by the two 8-pixel stores of a lane), k_agg3's TMA reads 64-byte runs.
+// G = 8 (-DHGF_WG8=1): the 32 labels of a warp store 1 KB of whole lines per instruction, k_agg3's TMA
+// reads 32-byte runs (profiles/r01_tma_run_rate.txt: ~1 run per clock per SM for either length).
+#ifndef HGF_WG8
+#define HGF_WG8 0
+#endif
+constexpr int kWGroupPx = HGF_WG8 ? 8 : 16, kWGroupLabels = 32;
 // Suspend-time hint (ns) for mbarrier.try_wait: a waiting warp is parked until the phase completes (or
 // the hint elapses) instead of spinning through issue slots the working warps need.
 constexpr unsigned kMbarSuspendNs = 20000;

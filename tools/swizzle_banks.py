@@ -1,4 +1,4 @@
-"""Shared-memory bank check for k_agg3's tile under the 64-byte TMA swizzle (IL layout) and the planar
+"""Shared-memory bank check for k_agg3's tile under the 64-byte (IL) / 32-byte (IL8, HGF_WG8) TMA swizzle and the planar
 odd-pitch tile: counts wavefronts per quarter-warp for the owner LDS.128 pattern and ways per warp for the
 vertical pass.  Usage: python tools/swizzle_banks.py [R]
 """
@@ -11,7 +11,14 @@ def swz(f):
     return f ^ ((f >> 3) & 12)
 
 
+def swz32(f):
+    """32-byte TMA swizzle (8-pixel groups, HGF_WG8; measured by tools/tma_swz8.cu)."""
+    return f ^ ((f >> 3) & 4)
+
+
 def owner(ln, wq, il):
+    if il == 2:
+        return (ln >> 3) + 4 * wq, ln & 7
     if il:
         return (ln & 3) + 4 * wq, ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1)
     return (ln & 7) + 8 * (wq % 3), (ln >> 3) + 4 * (wq // 3)
@@ -33,10 +40,10 @@ def main():
     K = 7
     WX, BY = TX + 2 * R, TY + 2 * R
     nv4 = (KX + 2 * R + 3) // 4
-    for il in (False, True):
+    for il in (0, 1, 2):
         if il:
             BX = (WX + 31) // 32 * 32
-            f = swz
+            f = swz if il == 1 else swz32
         else:
             BX = (WX + 3) // 4 * 4
             while (BX // 4) % 2 == 0:
@@ -60,7 +67,7 @@ def main():
                     a = f((k * BY + y) * BX + c)
                     banks.setdefault(a % 32, set()).add(a // 32)
                 vworst = max(vworst, max(len(v) for v in banks.values()))
-        print(f"R={R} {'IL/swizzle64' if il else 'planar'}: BX={BX} owner LDS.128 worst {worst} wavefronts "
+        print(f"R={R} {['planar', 'IL/swizzle64', 'IL8/swizzle32'][il]}: BX={BX} owner LDS.128 worst {worst} wavefronts "
               f"(ideal 4); vertical pass worst {vworst}-way")
 
 
