@@ -239,6 +239,15 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
       !fn || q != cudaDriverEntryPointSuccess)
     return false;
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  // HGF_TMA_L2PROMO = none | 64 | 128 (default) | 256: L2 sector promotion of the coefficient-tile loads
+  // (tuning knob for the interleaved layouts, whose inner runs are 32 or 64 bytes)
+  auto wmap_l2_promotion = [] {
+    const char* e = std::getenv("HGF_TMA_L2PROMO");
+    if (e && !strcmp(e, "none")) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    if (e && !strcmp(e, "64")) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    if (e && !strcmp(e, "256")) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  };
   int bx = 0, by = 0;
   hgf::agg3_box(h->r, h->wlay.il, &bx, &by);
   const int K = h->n + 1, KA = hgf::agg3_ka(K);
@@ -256,8 +265,7 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
       r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 hgf::kWGroupPx == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
-                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 hgf::kWGroupPx == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, wmap_l2_promotion(),
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
