@@ -81,6 +81,102 @@ __global__ void __launch_bounds__(SEG) k_stereo_cost(const float* __restrict__ b
   }
 }
 
+// k_stereo_cost4: the same cost, 4 consecutive pixels per thread (512-pixel row segments, 128 threads).  Per
+// label a thread loads one new column of the other view per plane and slides the other three in registers
+// (the 4 pixels' matches at disparity d + 1 are their matches at d shifted by one column), and writes the 4
+// costs with one 16-byte store: 1 shared load per plane and 1/4 store per voxel instead of 4 loads and 1 store
+// (k_stereo_cost).  Requires W % 4 == 0 (16-byte aligned rows); the arithmetic per voxel is k_stereo_cost's.
+constexpr int SEG4 = 512, T4 = SEG4 / 4;
+
+// The label loop of k_stereo_cost4.  The colour term a min(mean_c |.|, t_c) is evaluated as
+// (a/3) min(sum_c |.|, 3 t_c) (one multiply instead of a division; within an ulp of the literal form).
+template <int DIR, bool CHECK>
+__device__ __forceinline__ void cost4_labels(float (&w)[4][4], const float (&lr)[4], const float (&lg)[4],
+                                             const float (&lb)[4], const float (&lgr)[4], const float* rs, int span,
+                                             int ib, int xb, int d0, int Lc, int W, long long HW, float a, float tc,
+                                             float tg, float* out) {
+  const float trunc = a * tc + (1.0f - a) * tg;
+  const float a3 = a / 3.0f, tc3 = 3.0f * tc, ag = 1.0f - a;
+#pragma unroll 2
+  for (int k = 0; k < Lc; ++k) {
+    if (k > 0) {
+      if (DIR > 0) {
+        const int i = ib - k;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          w[c][3] = w[c][2]; w[c][2] = w[c][1]; w[c][1] = w[c][0];
+          w[c][0] = rs[c * span + i];
+        }
+      } else {
+        const int i = ib + k + 3;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          w[c][0] = w[c][1]; w[c][1] = w[c][2]; w[c][2] = w[c][3];
+          w[c][3] = rs[c * span + i];
+        }
+      }
+    }
+    float cv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float col = (fabsf(lr[j] - w[0][j]) + fabsf(lg[j] - w[1][j])) + fabsf(lb[j] - w[2][j]);
+      const float grd = fabsf(lgr[j] - w[3][j]);
+      float c = fmaf(a3, fminf(col, tc3), ag * fminf(grd, tg));
+      if (CHECK) {
+        const int xo = xb + j - DIR * (d0 + k);
+        if (xo < 0 || xo >= W) c = trunc;
+      }
+      cv[j] = c;
+    }
+    *reinterpret_cast<float4*>(out) = make_float4(cv[0], cv[1], cv[2], cv[3]);
+    out += HW;
+  }
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(T4) k_stereo_cost4(const float* __restrict__ base, const float* __restrict__ other,
+                                                     const float* __restrict__ gb, const float* __restrict__ go,
+                                                     float* __restrict__ cost, int W, int H, int d0, int Lc,
+                                                     float a, float tc, float tg) {
+  extern __shared__ float rs[];                    // [4][SEG4 + Lc + 3]: other view r, g, b, dx of its mean
+  const int y = blockIdx.y, x0 = blockIdx.x * SEG4, xb = x0 + 4 * threadIdx.x;
+  const long long HW = (long long)W * H, row = (long long)y * W;
+  const int span = SEG4 + Lc + 3;
+  // image column of rs[.][0]: the smallest column any (pixel, disparity) of the CTA reads, minus one slack column
+  const int xr0 = DIR > 0 ? x0 - d0 - Lc : x0 + d0 - 1;
+  for (int i = threadIdx.x; i < span; i += T4) {
+    const int xr = xr0 + i;
+    const bool in = xr >= 0 && xr < W;
+    rs[i] = in ? __ldg(other + row + xr) : 0.0f;
+    rs[span + i] = in ? __ldg(other + HW + row + xr) : 0.0f;
+    rs[2 * span + i] = in ? __ldg(other + 2 * HW + row + xr) : 0.0f;
+    rs[3 * span + i] = in ? __ldg(go + row + xr) : 0.0f;
+  }
+  __syncthreads();
+  if (xb >= W) return;
+  const float4 r4 = __ldg(reinterpret_cast<const float4*>(base + row + xb));
+  const float4 g4 = __ldg(reinterpret_cast<const float4*>(base + HW + row + xb));
+  const float4 b4 = __ldg(reinterpret_cast<const float4*>(base + 2 * HW + row + xb));
+  const float4 d4 = __ldg(reinterpret_cast<const float4*>(gb + row + xb));
+  const float lr[4] = {r4.x, r4.y, r4.z, r4.w}, lg[4] = {g4.x, g4.y, g4.z, g4.w};
+  const float lb[4] = {b4.x, b4.y, b4.z, b4.w}, lgr[4] = {d4.x, d4.y, d4.z, d4.w};
+  // window w[.][j] = other-view column of pixel xb + j at the current disparity d0 + k:
+  // DIR > 0: xb + j - d (index ib + j - k), DIR < 0: xb + j + d (index ib + j + k)
+  const int ib = DIR > 0 ? xb - d0 - xr0 : xb + d0 - xr0;
+  float w[4][4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[c][j] = rs[c * span + ib + j];
+  float* out = cost + row + xb;
+  // interior CTAs (every match column inside the image for every label) skip the per-voxel bounds test
+  const bool interior = DIR > 0 ? x0 - d0 - (Lc - 1) >= 0 : x0 + SEG4 - 1 + d0 + Lc - 1 < W;
+  if (interior)
+    cost4_labels<DIR, false>(w, lr, lg, lb, lgr, rs, span, ib, xb, d0, Lc, W, HW, a, tc, tg, out);
+  else
+    cost4_labels<DIR, true>(w, lr, lg, lb, lgr, rs, span, ib, xb, d0, Lc, W, HW, a, tc, tg, out);
+}
+
 }  // namespace
 
 cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cudaStream_t st) {
@@ -93,6 +189,20 @@ cudaError_t launch_stereo_grad(const float* img, float* grad, int W, int H, cuda
 cudaError_t launch_stereo_cost(const float* base, const float* other, const float* gb, const float* go, float* cost,
                                int W, int H, int d0, int Lc, int dir, float a, float tc, float tg, cudaStream_t st) {
   if (Lc < 1) return cudaSuccess;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (W % 4 == 0 && Lc <= 4096 && al16(base) && al16(gb) && al16(cost)) {
+    const size_t smem4 = sizeof(float) * 4 * (size_t)(SEG4 + Lc + 3);
+    if (smem4 <= 200 * 1024) {
+      auto kern = dir > 0 ? k_stereo_cost4<1> : k_stereo_cost4<-1>;
+      if (smem4 > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+        if (e != cudaSuccess) return e;
+      }
+      dim3 grid4((W + SEG4 - 1) / SEG4, H);
+      kern<<<grid4, T4, smem4, st>>>(base, other, gb, go, cost, W, H, d0, Lc, a, tc, tg);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = sizeof(float) * 4 * (size_t)(SEG + Lc - 1);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {

@@ -253,7 +253,9 @@ def test_prepared_path_unsupported_config_fails_loudly():
 
 
 @pytest.mark.parametrize("W,H,L,label_offset,d,r,mode", [(150, 90, 24, 0, 2, 9, "hgf"), (97, 61, 40, 5, 1, 4, "gf"),
-                                                          (64, 48, 8, 0, 1, 2, "hgf")])
+                                                          (64, 48, 8, 0, 1, 2, "hgf"),
+                                                          # W % 4 == 0: k_stereo_cost4, two 512-px segments
+                                                          (640, 40, 70, 9, 2, 9, "hgf")])
 def test_stereo_wta_parity(W, H, L, label_offset, d, r, mode):
     """NEXT-2: cost slices built on the GPU from the two views, then aggregation + WTA, against the
     oracle's own stereo cost filtered by the oracle."""

@@ -25,7 +25,8 @@ def _hgf(W, H, m, d, r, lam, mode="hgf"):
     return HGF(W, H, m, d, r, lam, mode=mode)
 
 
-@pytest.mark.parametrize("W,H,L,label_offset,d,r,mode", [(96, 64, 16, 0, 2, 4, "hgf"), (77, 45, 12, 3, 1, 3, "gf")])
+@pytest.mark.parametrize("W,H,L,label_offset,d,r,mode", [(96, 64, 16, 0, 2, 4, "hgf"), (77, 45, 12, 3, 1, 3, "gf"),
+                                                          (600, 36, 50, 7, 2, 5, "hgf")])
 def test_stereo_wta_right_parity(W, H, L, label_offset, d, r, mode):
     """P1: the right view's slices built on the GPU (match at x + d), filtered with the right view as guide,
     against the oracle's right-view cost filtered by the oracle."""
