@@ -434,3 +434,27 @@ def test_peer_merge_double_buffered_steps():
     assert pm.steps == 5
     pm.close()
     h.close()
+
+
+@pytest.mark.parametrize("promo", ["none", "64", "256"])
+def test_tma_l2_promotion_knob_is_bit_identical(promo, monkeypatch):
+    """HGF_TMA_L2PROMO only changes the cache policy of k_agg3's coefficient-tile loads: the filtered costs
+    and labels are bit-identical to the default (128-byte promotion) on the interleaved k_coef3 -> k_agg3
+    path (W multiple of 16, n = 6, r = 9, 40 labels: two 32-label groups, a ragged one)."""
+    torch = _torch()
+    W, H, L = 208, 72, 40
+    scene = synth.make_stereo_scene(W, H, L, seed=77)
+    g = torch.from_numpy(scene.left).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    monkeypatch.delenv("HGF_TMA_L2PROMO", raising=False)
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    a = h.aggregate_wta_ex(g, vol, labels=True, filtered=True)
+    torch.cuda.synchronize()
+    h.close()
+    monkeypatch.setenv("HGF_TMA_L2PROMO", promo)
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    b = h.aggregate_wta_ex(g, vol, labels=True, filtered=True)
+    torch.cuda.synchronize()
+    h.close()
+    assert torch.equal(a["filtered"], b["filtered"])
+    assert torch.equal(a["labels"], b["labels"])
