@@ -337,10 +337,27 @@ cudaError_t coef3_r(const void* tm_vol, const void* tm_g, const float* stats, fl
   using Gm = CoefGeom<NC>;
   cudaError_t e = cudaFuncSetAttribute(k_coef3<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
   if (e != cudaSuccess) return e;
-  // band height: enough CTAs to fill 148 SMs at least ~4 times, but long enough to amortise the warm-up
+  // band height: one CTA per SM (223 KB of SMEM), each band of BH rows costs BH + 2r row steps (the 2r-row
+  // warm-up of the vertical sums), so pick the band count nb (balanced bands of ceil(H / nb) >= 32 rows)
+  // minimising waves x (BH + 2r), waves = ceil(CTAs / 148), among the band counts that give at least 8
+  // waves (fewer, longer CTAs measured slower: BH = 360 at C4) or, for small images, the most CTAs.
+  // C4: nb = 8 (BH = 270, 12.97 waves) instead of BH = 128 (27.6 waves, 14 % warm-up): k_coef3
+  // 22.97 -> 22.24 ms (HGF_COEF3_BH sweep, profiles/r01_coef3_bh_sweep.txt).
   const int strips = (W + C_TX - 1) / C_TX, batches = (L + Gm::LB - 1) / Gm::LB;
-  int BH = 128;
-  while (BH > 32 && (long long)strips * ((H + BH - 1) / BH) * batches < 4 * 148) BH /= 2;
+  int BH = H;
+  {
+    long long best = -1;
+    const int nbmax = H / 32 > 1 ? H / 32 : 1;
+    const long long most = (long long)strips * ((H + (H + nbmax - 1) / nbmax - 1) / ((H + nbmax - 1) / nbmax)) * batches;
+    const long long target = most < 8 * 148 ? most : 8 * 148;
+    for (int nb = 1; nb <= nbmax; ++nb) {
+      const int bh = (H + nb - 1) / nb;
+      const long long ctas = (long long)strips * ((H + bh - 1) / bh) * batches;
+      if (ctas < target) continue;
+      const long long cost = (ctas + 147) / 148 * (bh + 2 * r);
+      if (best < 0 || cost < best) { best = cost; BH = bh; }
+    }
+  }
   static const int bh_env = std::getenv("HGF_COEF3_BH") ? std::atoi(std::getenv("HGF_COEF3_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning runs only
   dim3 grid(strips, (H + BH - 1) / BH, batches);
