@@ -21,6 +21,7 @@ struct hgf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   float* G = nullptr;          // [n][H][W]     polynomial guidance (K1)
+  float* Gp = nullptr;         // [H][m][W][2]  (I_i, I_i^2) pairs for k_coef5 when d = 2 (K1)
   float* stats = nullptr;      // [NS][H][W]    P' upper triangle + nu (K3)
   float* wbuf = nullptr;       // [lcap][n+1][H][W] per-slice coefficients w (K4a -> K4b)
   int lcap = 0;                // labels per coefficient chunk
@@ -50,6 +51,8 @@ struct hgf_ctx {
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
   bool v4coef = false;         // tensor-core coefficient kernel (planar layout for k_agg3, n <= 6, r <= 9)
+  bool v5coef = false;         // horizontal-first coefficient kernel (interleaved layout, n <= 6, r <= 9): default
+  CUtensorMap tm_g5;           // TMA descriptor over the raw guide planes of G for k_coef5 (box 164 x 1 x m)
   CUtensorMap tm_g4;           // TMA descriptor over G for k_coef4 (box kCoef4BoxX x 1 x n)
   CUtensorMap tm_g;            // TMA descriptor over G (dims W, H, n; box 88 x 1 x n) for k_coef3
   std::string err;
@@ -120,6 +123,7 @@ void release(hgf_ctx* h) {
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
   h->pool.clear();
   cudaFree(h->G);
+  cudaFree(h->Gp);
   cudaFree(h->stats);
   cudaFree(h->wbuf);
   cudaFree(h->best_cost);
@@ -156,13 +160,14 @@ hgf_status check_async(hgf_ctx* h) {
 // Steps 1-2: polynomial guidance (all rows) and the statistics of rows [y0, y1).
 hgf_status frame_stats(hgf_ctx* h, const float* guide, int y0, int y1) {
   cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
-    return hgf::launch_poly_guidance(guide, h->G, h->m, h->d, h->W, h->H, h->stream);
+    return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->m, h->d, h->W, h->H, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
     const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
     return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode,
-                             (h->v3coef || h->v4coef) ? 1 : 0, lam0, y0, y1, h->st3_scratch, h->stream);
+                             (h->v3coef || h->v4coef || h->v5coef) ? 1 : 0, lam0, y0, y1, h->st3_scratch,
+                             h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
   return HGF_OK;
@@ -195,6 +200,21 @@ bool encode_map_3d(CUtensorMap* tm, const void* base, long long dx, long long dy
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D tensor map over 8-byte elements (the (I, I^2) guide pairs of k_coef5): dims (dx, dy, dz), row pitch and
+// plane stride in ELEMENTS, zero fill out of bounds.
+bool encode_map_3d_u64(CUtensorMap* tm, const void* base, long long dx, long long dy, long long dz, long long pitch,
+                       long long plane, int bx, int by, int bz) {
+  auto encode = tensor_map_encoder();
+  if (!encode || ((uintptr_t)base & 15) || ((pitch * 8) & 15) || ((plane * 8) & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)dx, (cuuint64_t)dy, (cuuint64_t)dz};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)plane * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // K4a for one chunk of Lc slices: the v2 fast path when (m, d, r) allow it, else the generic v1 kernel.
 cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
@@ -205,6 +225,15 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
                          hgf::kCoef4BoxX, 1, hgf::kCoef4LB))
         return cudaErrorInvalidValue;
       return hgf::launch_coef_v4(h->n, &tm_vol, &h->tm_g4, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc,
+                                 h->stream);
+    }
+    if (h->v5coef) {
+      // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 164 x 1 x 32 (k_coef5)
+      CUtensorMap tm_vol;
+      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, hgf::kCoef5BoxX,
+                         1, hgf::kCoef5LB))
+        return cudaErrorInvalidValue;
+      return hgf::launch_coef_v5(h->m, h->d, &tm_vol, &h->tm_g5, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc,
                                  h->stream);
     }
     if (h->v3coef) {
@@ -386,6 +415,21 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     const char* f = std::getenv("HGF_COEF3");
     h->v3coef = !h->v4coef && h->v3agg && h->n <= hgf::kCoef3MaxN && (W % 4) == 0 && !(f && f[0] == '0') &&
                 encode_map_3d(&h->tm_g, h->G, W, H, h->n, W, (long long)W * H, 88, 1, h->n);
+    // k_coef5 (default where it applies; HGF_COEF5=0 keeps k_coef3): same interleaved layout as k_coef3
+    const char* f5 = std::getenv("HGF_COEF5");
+    // tm_g5: d = 2: the (I_i, I_i^2) pairs [H][m][W] as 8-byte elements, dims (W, m, H); other degrees: the raw
+    // guide channels I_i = G_{(i-1)d+1} (every d-th plane of the guidance buffer), dims (W, H, m)
+    h->v5coef = h->v3coef && hgf::coef5_ok(h->m, h->d, h->r) && !(f5 && f5[0] == '0');
+    if (h->v5coef && h->d == 2) {
+      if (cudaMalloc(&h->Gp, sizeof(float) * 2 * h->m * HW) != cudaSuccess) {
+        cudaGetLastError();
+        h->Gp = nullptr;
+      }
+      h->v5coef = h->Gp && encode_map_3d_u64(&h->tm_g5, h->Gp, W, h->m, H, W, (long long)W * h->m, hgf::kCoef5BoxX,
+                                             h->m, 1);
+    } else if (h->v5coef) {
+      h->v5coef = encode_map_3d(&h->tm_g5, h->G, W, H, h->m, W, (long long)W * H * h->d, hgf::kCoef5BoxX, 1, h->m);
+    }
   }
   // coefficient buffer layout: label-interleaved for k_coef3 -> k_agg3, else rows pitched to a multiple of
   // 4 floats for the TMA aggregation, else flat
@@ -430,6 +474,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->v3agg = false;
     h->v3coef = false;
     h->v4coef = false;
+    h->v5coef = false;
     h->wlay = flat;
   }
   *out = h;

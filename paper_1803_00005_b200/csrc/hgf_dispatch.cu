@@ -8,7 +8,9 @@
 namespace hgf {
 
 // ------------------------------------------------------------------ K1: polynomial guidance
-__global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__ G, int m, int d, long long HW) {
+// Gp (optional, d = 2): the same powers as (I_i, I_i^2) pairs, layout [H][m][W][2] (k_coef5's guide rows).
+__global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__ G, float2* __restrict__ Gp, int m, int d,
+                                int W, long long HW) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
     for (int i = 0; i < m; ++i) {
       const float v = I[i * HW + p];
@@ -17,6 +19,10 @@ __global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__
       for (int j = 1; j < d; ++j) {
         t = t * v;
         G[(long long)(i * d + j) * HW + p] = t;
+      }
+      if (Gp) {
+        const long long y = p / W, x = p - y * W;
+        Gp[(y * m + i) * W + x] = make_float2(v, v * v);
       }
     }
   }
@@ -42,9 +48,10 @@ static int grid_1d(long long n, int threads) {
   return (int)(b < 148LL * 32 ? (b < 1 ? 1 : b) : 148LL * 32);
 }
 
-cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st) {
+cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int m, int d, int W, int H, cudaStream_t st) {
   const long long HW = (long long)W * H;
-  k_poly_guidance<<<grid_1d(HW, 256), 256, 0, st>>>(I, G, m, d, HW);
+  k_poly_guidance<<<grid_1d(HW, 256), 256, 0, st>>>(I, G, reinterpret_cast<float2*>(d == 2 ? Gp : nullptr), m, d, W,
+                                                      HW);
   return cudaGetLastError();
 }
 

@@ -27,7 +27,8 @@ struct AggArgs {
   int rows_per_owner;
 };
 
-cudaError_t launch_poly_guidance(const float* I, float* G, int m, int d, int W, int H, cudaStream_t st);
+// Gp (nullable; used when d == 2): (I_i, I_i^2) pairs, layout [H][m][W][2], for k_coef5.
+cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int m, int d, int W, int H, cudaStream_t st);
 // aos = 1: per-pixel records of kStatsAos floats (statistics, then kappa = 1/(lam0f + N)) for k_coef3;
 // needs the k_stats2 path (else cudaErrorInvalidValue).
 // Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).
@@ -125,6 +126,14 @@ cudaError_t coef4_impl(const void* tm_vol, const void* tm_g, const float* stats,
 }  // namespace v4
 cudaError_t launch_coef_v4(int n, const void* tm_vol, const void* tm_g, const float* stats, float* wbuf, WLayout wo,
                            int W, int H, int r, int L, cudaStream_t st);
+// Horizontal-first coefficient kernel (hgf_coef_v5.cuh, instantiated in hgf_coef5.cu): raw guide channels
+// m <= 3, degree d <= 3, n = m d <= 6, r <= 9, label-interleaved layout, per-pixel statistics records.
+// tm_vol: box kCoef5BoxX x 1 x kCoef5LB over the chunk's slices; tm_i: box kCoef5BoxX x 1 x m over the raw
+// guide channels (the planes G_{(i-1)d+1} = I_i of the guidance buffer).
+constexpr int kCoef5BoxX = 164, kCoef5LB = 32, kCoef5MaxN = 6;
+bool coef5_ok(int m, int d, int r);
+cudaError_t launch_coef_v5(int m, int d, const void* tm_vol, const void* tm_i, const float* stats, float* wbuf,
+                           WLayout wo, int W, int H, int r, int L, cudaStream_t st);
 }  // namespace hgf
 
 namespace hgf {
