@@ -259,6 +259,11 @@ HGF_API hgf_status hgf_profile_read(hgf_handle h, double* ms, int* counts, int n
 /* Number of kernel launches the last hgf_filter / hgf_aggregate_wta* call enqueued. */
 HGF_API int hgf_last_launch_count(hgf_handle h);
 
+/* The slice-kernel pair this handle runs, fixed at create time from (W, H, n_guide, poly_degree, radius)
+ * and the HGF_* selection variables: "coef5+agg3" (default for m <= 3, d <= 3, n <= 6, r <= 9, W % 4 == 0),
+ * "coef3+agg3", "coef4+agg3", "coef2+agg3", "coef2+agg2", "coef1+agg1".  Static string; NULL handle -> "". */
+HGF_API const char* hgf_kernel_path(hgf_handle h);
+
 /* Static description of a status code. */
 HGF_API const char* hgf_status_string(hgf_status s);
 

@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "hgf_prepare_rows", "hgf_stats_buffer", "hgf_aggregate_wta_prepared", "hgf_stereo_wta", "hgf_segment",
     "hgf_aggregate_wta_peer", "hgf_fill_keys", "hgf_unpack_keys_n", "hgf_alloc", "hgf_free", "hgf_ipc_get_handle",
     "hgf_ipc_open", "hgf_ipc_close", "hgf_stereo_wta_right", "hgf_lr_postprocess", "hgf_stereo_disparity",
+    "hgf_kernel_path",
 )
 KERNEL_CLASSES = ("guidance", "stats", "coef", "agg", "keys", "cost", "post")   # HGF_KC_* order
 
@@ -57,6 +58,8 @@ def lib():
     L.hgf_aggregate_wta_host.argtypes = [vp, vp, vp, c_int, vp]
     L.hgf_last_launch_count.argtypes = [vp]
     L.hgf_last_launch_count.restype = c_int
+    L.hgf_kernel_path.argtypes = [vp]
+    L.hgf_kernel_path.restype = ctypes.c_char_p
     L.hgf_status_string.argtypes = [c_int]
     L.hgf_status_string.restype = ctypes.c_char_p
     L.hgf_last_error.argtypes = [vp]
@@ -151,6 +154,11 @@ class HGF:
     @property
     def last_launch_count(self):
         return lib().hgf_last_launch_count(self._h)
+
+    @property
+    def kernel_path(self):
+        """The slice kernels this handle runs (hgf_kernel_path), e.g. "coef5+agg3"."""
+        return lib().hgf_kernel_path(self._h).decode()
 
     # ------------------------------------------------------------------ API (names as in hgf.h)
     def filter(self, guide, src, dst=None):

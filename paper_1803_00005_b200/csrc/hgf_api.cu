@@ -376,6 +376,17 @@ const char* hgf_last_error(hgf_handle h) { return h ? h->err.c_str() : "null han
 
 int hgf_last_launch_count(hgf_handle h) { return h ? h->launches : 0; }
 
+const char* hgf_kernel_path(hgf_handle h) {
+  if (!h) return "";
+  if (h->v3agg) {
+    if (h->v5coef) return "coef5+agg3";
+    if (h->v4coef) return "coef4+agg3";
+    if (h->v3coef) return "coef3+agg3";
+    return "coef2+agg3";
+  }
+  return h->fast ? "coef2+agg2" : "coef1+agg1";
+}
+
 hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_degree, int radius, double eps,
                          int mode, void* cuda_stream) {
   if (!out) return HGF_ERR_INVALID_ARGUMENT;

@@ -25,3 +25,22 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Parity margins of every GPU check (tests/parity_util.MARGINS), printed even when all tests pass."""
+    try:
+        from tests.parity_util import MARGINS
+    except Exception:  # pragma: no cover
+        return
+    if not MARGINS:
+        return
+    tr = terminalreporter
+    tr.write_sep("-", "parity margins (quantity, value, bound)")
+    for tag, q, v, b in MARGINS:
+        tr.write_line(f"{tag}  {q} {v:.3e}" + (f" (bound {b:g})" if b is not None else " (per-pixel rules only)"))
+    errs = [v for _, q, v, _ in MARGINS if q == "max_norm_err"]
+    agr = [v for _, q, v, b in MARGINS if q == "label_agreement"]
+    if errs:
+        tr.write_line(f"worst max normalised error {max(errs):.3e} of 1e-4 over {len(errs)} checks; "
+                      f"lowest label agreement {min(agr) if agr else float('nan'):.6f}")

@@ -1,18 +1,31 @@
-"""Parity rules (SURVEY §8(c), DESIGN.md §6) shared by the GPU tests and smoke().
+"""Parity rules (SURVEY §8(c), DESIGN.md §7) shared by the GPU tests and smoke().
 
 Filtered costs:  e(p,l) = |Z_gpu - Z_ora| / max(|Z_ora|, 1e-3 s_V) <= 1e-4, s_V = max|V|
                  (BASELINE.json north_star: "max relative error 1e-4 (fp32 against fp64)"; a pure
                  relative error is ill-posed where Z -> 0, hence the 1e-3 s_V floor).
-Labels:          bit-exact wherever the oracle's top-two gap (Z_(2)-Z_(1)) / max(|Z_(1)|, 1e-3 s_V)
-                 exceeds 1e-4, and agreement >= 99.99 % overall.
-"""
-import os
+Labels:          (1) bit-exact wherever the oracle's top-two gap (Z_(2)-Z_(1)) / max(|Z_(1)|, 1e-3 s_V)
+                     exceeds 1e-4;
+                 (2) at the remaining (near-tie) pixels the GPU's label must be near-optimal: its oracle
+                     cost lies within 1e-4 (same normalisation) of the oracle's minimum;
+                 (3) agreement >= 99.99 % overall, checked on every case of >= 10^4 pixels (below that a
+                     single near-tie flip is already > 0.01 %, and rule (2) is the per-pixel check).
 
+Every check records its margin (max normalised error, agreement, near-tie share) in MARGINS; the
+conftest prints them at the end of the session so they land in the GPU test log even when all pass.
+"""
 import numpy as np
 
 Z_TOL = 1e-4
 GAP = 1e-4
 AGREE = 0.9999
+AGREE_MIN_PIXELS = 10_000
+
+MARGINS = []          # (test id or tag, quantity, value, bound)
+
+
+def _tag():
+    import os
+    return os.environ.get("PYTEST_CURRENT_TEST", "smoke").split(" ")[0]
 
 
 def z_error(z_gpu, z_ora, s_v):
@@ -26,24 +39,33 @@ def check_z(z_gpu, z_ora, s_v, tol=Z_TOL):
     e = z_error(z_gpu, z_ora, s_v)
     assert np.all(np.isfinite(np.asarray(z_gpu))), "non-finite GPU output"
     worst = float(e.max()) if e.size else 0.0
-    if os.environ.get("HGF_PARITY_REPORT"):
-        print(f"[parity] max normalised error {worst:.3e} (tol {tol:.0e})")
+    MARGINS.append((_tag(), "max_norm_err", worst, tol))
+    print(f"[parity] max normalised error {worst:.3e} (tol {tol:.0e})")
     assert worst <= tol, f"max relative error {worst:.3e} > {tol:.1e}"
     return worst
 
 
 def check_labels(lab_gpu, Z_ora, s_v):
-    """Z_ora: (L, H, W) oracle filtered costs."""
+    """Z_ora: (L, H, W) oracle filtered costs; lab_gpu relative to slice 0.  Returns (agreement, near-tie share)."""
     lab_gpu = np.asarray(lab_gpu)
     lab_ora = np.argmin(Z_ora, axis=0)            # lowest index on ties
     if Z_ora.shape[0] >= 2:
         srt = np.sort(Z_ora, axis=0)
-        gap = (srt[1] - srt[0]) / np.maximum(np.abs(srt[0]), 1e-3 * s_v)
-        clear = gap > GAP
+        den = np.maximum(np.abs(srt[0]), 1e-3 * s_v)
+        clear = (srt[1] - srt[0]) / den > GAP
+        # (2) near-optimality of every GPU label (trivially true where it equals the oracle's)
+        assert lab_gpu.min() >= 0 and lab_gpu.max() < Z_ora.shape[0], "label out of range"
+        zg = np.take_along_axis(Z_ora, lab_gpu[None].astype(np.int64), axis=0)[0]
+        worst_tie = float(((zg - srt[0]) / den).max())
+        assert worst_tie <= GAP, f"a GPU label's oracle cost is {worst_tie:.2e} above the minimum (> {GAP})"
     else:
         clear = np.ones(lab_ora.shape, dtype=bool)
     mism_clear = int(np.count_nonzero((lab_gpu != lab_ora) & clear))
     agree = float(np.mean(lab_gpu == lab_ora))
+    near = float(np.mean(~clear))
+    MARGINS.append((_tag(), "label_agreement", agree, AGREE if lab_gpu.size >= AGREE_MIN_PIXELS else None))
+    print(f"[parity] label agreement {agree:.6f}, near-tie share {near:.5f}, {lab_gpu.size} px")
     assert mism_clear == 0, f"{mism_clear} label mismatches where the oracle gap > {GAP}"
-    assert agree >= AGREE, f"label agreement {agree:.6f} < {AGREE}"
-    return agree, float(np.mean(~clear))
+    if lab_gpu.size >= AGREE_MIN_PIXELS:
+        assert agree >= AGREE, f"label agreement {agree:.6f} < {AGREE}"
+    return agree, near

@@ -458,3 +458,84 @@ def test_tma_l2_promotion_knob_is_bit_identical(promo, monkeypatch):
     h.close()
     assert torch.equal(a["filtered"], b["filtered"])
     assert torch.equal(a["labels"], b["labels"])
+
+
+# Full frames on the default slice path at the geometry bench.py runs (verdict r01 item 2b): >= 3 strips, >= 3 row
+# bands, >= 2 label batches, and the C4 band length (270 rows: the fp32 running window sums of a band march 288
+# steps without a restart), with the stereo-like and the iid near-tie distributions; k_coef3 at the same band length.
+BAND_CASES = [
+    # (name, W, H, L, distribution, env, expected kernel path)
+    ("coef5-3strips-3bands-2batches", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
+    ("coef5-iid-band270", 260, 560, 34, "iid", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
+    ("coef3-band270", 300, 560, 40, "stereo", {"HGF_COEF5": "0", "HGF_COEF3_BH": "270"}, "coef3+agg3"),
+]
+
+
+@pytest.mark.parametrize("name,W,H,L,dist,env,path", BAND_CASES, ids=[c[0] for c in BAND_CASES])
+def test_full_frame_band_geometry(monkeypatch, name, W, H, L, dist, env, path):
+    torch = _torch()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    if dist == "stereo":
+        scene = synth.make_stereo_scene(W, H, L, seed=300 + L)
+        I, V = scene.left, synth.stereo_cost_volume_np(scene, L)
+    else:
+        I, V = synth.iid_volume(W, H, L, 3, seed=301)
+    I, V = np.ascontiguousarray(I), np.ascontiguousarray(V)
+    h = _hgf(W, H, 3, 2, 9, 0.05)
+    assert h.kernel_path == path
+    out = h.aggregate_wta_ex(torch.from_numpy(I).cuda(), torch.from_numpy(V).cuda(), labels=True, min_cost=True,
+                             filtered=True)
+    torch.cuda.synchronize()
+    h.close()
+    Z = O.hgf_filter(I, V, 0.05, 9, 2)
+    s_v = float(np.abs(V).max())
+    check_z(out["filtered"].cpu().numpy(), Z, s_v)
+    check_labels(out["labels"].cpu().numpy(), Z, s_v)
+
+
+def test_default_kernel_path_is_coef5():
+    """The headline configs (RGB degree 2, r = 9, W % 4 == 0) run k_coef5 -> k_agg3 by default."""
+    for W, H in ((3840, 2160), (1920, 1080), (452, 375)):
+        h = _hgf(W, H, 3, 2, 9, 0.05)
+        assert h.kernel_path == "coef5+agg3", (W, H, h.kernel_path)
+        h.close()
+
+
+def test_shard_merge_against_oracle():
+    """A9 (label-sharded WTA merge, north_star (4)): three contiguous label shards, each through
+    hgf_aggregate_wta_ex(label_offset, keys), merged by elementwise int64 MIN and unpacked -- labels and
+    minimum cost against the ORACLE's argmin / min over the whole volume (not only against the unsharded run)."""
+    torch = _torch()
+    from paper_1803_00005_b200 import shard_range
+    W, H, L = 180, 77, 30
+    scene = synth.make_stereo_scene(W, H, L, seed=93)
+    V = synth.stereo_cost_volume_np(scene, L)
+    gi = torch.from_numpy(scene.left).cuda()
+    h = _hgf(W, H, 3, 2, 9, 0.05)
+    keys = None
+    for rank in range(3):
+        l0, l1 = shard_range(L, 3, rank)
+        part = h.aggregate_wta_ex(gi, torch.from_numpy(np.ascontiguousarray(V[l0:l1])).cuda(), label_offset=l0,
+                                  keys=True)["keys"]
+        keys = part if keys is None else torch.minimum(keys, part)
+    lab, cost = h.unpack_keys(keys)
+    # the same merge through the fused peer-memory path (two owners x two shards, one process)
+    R = (H + 1) // 2
+    owners = [torch.empty((R, W), dtype=torch.int64, device="cuda") for _ in range(2)]
+    for o in owners:
+        h.fill_keys(o)
+    ptrs = torch.tensor([o.data_ptr() for o in owners], dtype=torch.int64, device="cuda")
+    h.prepare_rows(gi, 0, H)
+    vol = torch.from_numpy(V).cuda()
+    for rank in range(2):
+        l0, l1 = shard_range(L, 2, rank)
+        h.aggregate_wta_peer(vol[l0:l1].contiguous(), ptrs, 2, R, label_offset=l0)
+    torch.cuda.synchronize()
+    peer_keys = torch.cat(owners)[:H]
+    h.close()
+    Z = O.hgf_filter(scene.left, V, 0.05, 9, 2)
+    s_v = float(np.abs(V).max())
+    check_labels(lab.cpu().numpy(), Z, s_v)
+    check_z(cost.cpu().numpy(), Z.min(axis=0), s_v)
+    assert torch.equal(peer_keys, keys)

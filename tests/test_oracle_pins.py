@@ -215,6 +215,59 @@ def test_filter_definition_vs_brute_vs_paper(mode, m, d, r, H, W):
     assert np.allclose(z_paper, z_def, rtol=1e-6, atol=1e-8)
 
 
+@pytest.mark.parametrize("mode", ["hgf", "gf"])
+@pytest.mark.parametrize("method", ["solve", "paper"])
+@pytest.mark.parametrize("m,d,r,H,W,L", [(3, 2, 2, 8, 10, 3), (1, 3, 1, 6, 5, 2), (2, 1, 3, 7, 9, 4)])
+def test_multislice_stack_equals_per_slice_and_brute(mode, method, m, d, r, H, W, L):
+    """The stacked (L, H, W) branches of hgf_weights / hgf_filter (the form every GPU parity test compares
+    against: the 4-D batched solve of the HGF mode, the GF mode's stacked centring cc = Gy - N mu ybar and
+    the w0 = ybar - sum_i w_i mu_i contraction, the per-slice Eq13 loop of method "paper") against
+    (a) hgf_filter_brute slice by slice -- explicit window gathers + LU + the explicit Eq8 double loop
+    (P:257-262), no box filter, no SAT, no batched solve -- and (b) the single-slice branch."""
+    rng = np.random.default_rng(1000 + 97 * m + 13 * d + r + L)
+    I = rng.random((m, H, W))
+    Y = rng.random((L, H, W))
+    lam = 0.05
+    z_stack = O.hgf_filter(I, Y, lam, r, d, mode=mode, method=method)
+    assert z_stack.shape == (L, H, W)
+    G = O.poly_guidance(I, d)
+    w_stack = O.hgf_weights(G, Y, lam, r, mode=mode, method=method)
+    assert w_stack.shape == (m * d + 1, L, H, W)
+    for l in range(L):
+        z_brute = O.hgf_filter_brute(I, Y[l], lam, r, d, mode=mode)
+        tol = (1e-9, 1e-10) if method == "solve" else (1e-6, 1e-8)
+        assert np.allclose(z_stack[l], z_brute, rtol=tol[0], atol=tol[1])
+        assert np.allclose(z_stack[l], O.hgf_filter(I, Y[l], lam, r, d, mode=mode, method=method), rtol=1e-12,
+                           atol=1e-13)
+        assert np.allclose(w_stack[:, l], O.hgf_weights(G, Y[l], lam, r, mode=mode, method=method), rtol=1e-12,
+                           atol=1e-13)
+
+
+def test_multislice_gf_centring_terms_written_out():
+    """GF mode's stacked centring (Eq16 P:369 via §5.1's centred regression): the stacked weights
+    equal the per-window textbook solve written out with explicit means -- w = (lam E + Xc^T Xc)^-1 Xc^T cc,
+    w0 = mean(c) - w^T mean(x) -- for every slice, so a transposed operand or a dropped N mu ybar term in the
+    stacked branch fails."""
+    rng = np.random.default_rng(77)
+    m, d, r, H, W, L, lam = 2, 2, 2, 6, 7, 3, 0.05
+    I = rng.random((m, H, W))
+    Y = rng.random((L, H, W))
+    G = O.poly_guidance(I, d)
+    w = O.hgf_weights(G, Y, lam, r, mode="gf")
+    n = m * d
+    for l in range(L):
+        for y in range(H):
+            for x in range(W):
+                ys = slice(max(0, y - r), min(H, y + r + 1))
+                xs = slice(max(0, x - r), min(W, x + r + 1))
+                X = np.stack([G[i][ys, xs].ravel() for i in range(n)], 1)
+                c = Y[l][ys, xs].ravel()
+                Xc, cc = X - X.mean(0), c - c.mean()
+                ws = np.linalg.solve(lam * np.eye(n) + Xc.T @ Xc, Xc.T @ cc)
+                assert np.allclose(w[1:, l, y, x], ws, rtol=1e-9, atol=1e-11)
+                assert np.isclose(w[0, l, y, x], c.mean() - ws @ X.mean(0), rtol=1e-9, atol=1e-11)
+
+
 def test_intercept_penalty_distinguishes_modes():
     """HGF (Eq7) penalises w(0); GF (Eq15) does not — a dropped/added intercept term changes Z."""
     I = RNG.random((3, 10, 10))
