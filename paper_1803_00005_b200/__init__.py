@@ -454,8 +454,9 @@ class PeerKeys:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.rows = -(-h.H // self.world)
-        self.y0 = self.rank * self.rows
-        self.y1 = min(h.H, self.y0 + self.rows)
+        # ranks past the last row (world > ceil(H / rows)) own an empty range, never a negative one
+        self.y0 = min(h.H, self.rank * self.rows)
+        self.y1 = max(self.y0, min(h.H, self.y0 + self.rows))
         nbytes = 8 * self.rows * h.W
         p = ctypes.c_void_p()
         st = lib().hgf_alloc(nbytes, ctypes.byref(p))

@@ -281,10 +281,11 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
       if (min_cost_out) min_cost_out[p] = best[s];
       if (keys_out) keys_out[p] = pack_key_signed(best[s], bl[s]);
       if (peer_keys) {
-        // fused merge: a 64-bit atomic MIN on the owner GPU's key buffer (over NVLink for remote owners)
+        // fused merge: a 64-bit atomic MIN on the owner GPU's key buffer (over NVLink for remote owners).
+        // System scope: the owners' buffers are written by several GPUs (ATOM.E.MIN.S64.STRONG.SYS).
         const int owner = gy / rows_per_owner;
-        atomicMin(peer_keys[owner] + (long long)(gy - owner * rows_per_owner) * W + gx,
-                  (long long)pack_key_signed(best[s], bl[s]));
+        atomicMin_system(peer_keys[owner] + (long long)(gy - owner * rows_per_owner) * W + gx,
+                         (long long)pack_key_signed(best[s], bl[s]));
       }
     } else {
       best_cost[p] = best[s];

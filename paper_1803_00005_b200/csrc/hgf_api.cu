@@ -65,6 +65,22 @@ struct hgf_ctx {
 
 namespace {
 
+// Every entry point that takes a handle runs on the handle's device (hgf.h: "bound to the CUDA device current
+// at create time"): switch to it for the call and restore the caller's current device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const hgf_ctx* h) {
+    if (h && cudaGetDevice(&prev) == cudaSuccess && prev != h->device) {
+      if (cudaSetDevice(h->device) != cudaSuccess) prev = -1;
+    } else {
+      prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 hgf_status fail(hgf_ctx* h, hgf_status s, const std::string& msg) {
   if (h) h->err = msg;
   return s;
@@ -497,6 +513,7 @@ hgf_status hgf_create(hgf_handle* out, int W, int H, int n_guide, int poly_degre
 }
 
 hgf_status hgf_destroy(hgf_handle h) {
+  DeviceGuard dg(h);
   if (!h) return HGF_OK;
   cudaStreamSynchronize(h->stream);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
@@ -512,6 +529,7 @@ hgf_status hgf_set_stream(hgf_handle h, void* cuda_stream) {
 }
 
 hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float* dst) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -525,6 +543,7 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
 
 hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* cost_volume, int L, int label_offset,
                                 int32_t* labels_out, float* min_cost_out, float* filtered_out, int64_t* keys_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -542,6 +561,7 @@ hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* c
 }
 
 hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -555,6 +575,7 @@ hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1) {
 }
 
 hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row) {
+  DeviceGuard dg(h);
   if (!h || !dev_ptr || !bytes_per_row) return HGF_ERR_INVALID_ARGUMENT;
   if (!(h->v3coef || h->v4coef))
     return fail(h, HGF_ERR_UNSUPPORTED, "statistics are not stored row-contiguously in this configuration");
@@ -566,6 +587,7 @@ hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row)
 hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, int L, int label_offset,
                                       int32_t* labels_out, float* min_cost_out, float* filtered_out,
                                       int64_t* keys_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -682,6 +704,7 @@ extern "C" {
 hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, int L, int label_offset,
                           float alpha, float tau_color, float tau_grad, int32_t* labels_out, float* min_cost_out,
                           float* filtered_out, int64_t* keys_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -692,6 +715,7 @@ hgf_status hgf_stereo_wta(hgf_handle h, const float* left, const float* right, i
 hgf_status hgf_stereo_wta_right(hgf_handle h, const float* left, const float* right, int L, int label_offset,
                                 float alpha, float tau_color, float tau_grad, int32_t* labels_out,
                                 float* min_cost_out, float* filtered_out, int64_t* keys_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -702,6 +726,7 @@ hgf_status hgf_stereo_wta_right(hgf_handle h, const float* left, const float* ri
 hgf_status hgf_lr_postprocess(hgf_handle h, const float* image, const int32_t* disp_left, const int32_t* disp_right,
                               int tol, int radius, float sigma_s, float sigma_c, uint8_t* valid_out,
                               int32_t* disp_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -716,6 +741,7 @@ hgf_status hgf_stereo_disparity(hgf_handle h, const float* left, const float* ri
                                 float alpha, float tau_color, float tau_grad, int tol, int radius, float sigma_s,
                                 float sigma_c, int32_t* disp_left_out, int32_t* disp_right_out, uint8_t* valid_out,
                                 int32_t* disp_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -737,6 +763,7 @@ hgf_status hgf_stereo_disparity(hgf_handle h, const float* left, const float* ri
 
 hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds, const uint8_t* bg_seeds,
                        int32_t* labels_out, float* min_cost_out, float* filtered_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -781,6 +808,7 @@ hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds
 
 hgf_status hgf_aggregate_wta_peer(hgf_handle h, const float* cost_volume, int L, int label_offset,
                                   int64_t* const* peer_keys_dev, int world, int rows_per_owner) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -803,6 +831,7 @@ hgf_status hgf_aggregate_wta_peer(hgf_handle h, const float* cost_volume, int L,
 }
 
 hgf_status hgf_fill_keys(hgf_handle h, int64_t* keys, long long n) {
+  DeviceGuard dg(h);
   if (!h || !keys || n < 0) return HGF_ERR_INVALID_ARGUMENT;
   cudaError_t e = hgf::launch_fill_i64(keys, n, (long long)0x7FFFFFFFFFFFFFFFLL, h->stream);
   return e == cudaSuccess ? HGF_OK : cuda_fail(h, e, "fill_keys");
@@ -810,6 +839,7 @@ hgf_status hgf_fill_keys(hgf_handle h, int64_t* keys, long long n) {
 
 hgf_status hgf_unpack_keys_n(hgf_handle h, const int64_t* keys, long long n, int32_t* labels_out,
                              float* min_cost_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -863,11 +893,13 @@ hgf_status hgf_ipc_close(void* dev_ptr) {
 }
 
 hgf_status hgf_aggregate_wta(hgf_handle h, const float* guide, const float* cost_volume, int L, int32_t* labels_out) {
+  DeviceGuard dg(h);
   if (!labels_out) return h ? fail(h, HGF_ERR_INVALID_ARGUMENT, "labels_out is null") : HGF_ERR_INVALID_ARGUMENT;
   return hgf_aggregate_wta_ex(h, guide, cost_volume, L, 0, labels_out, nullptr, nullptr, nullptr);
 }
 
 hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_out, float* min_cost_out) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -881,6 +913,7 @@ hgf_status hgf_unpack_keys(hgf_handle h, const int64_t* keys, int32_t* labels_ou
 
 hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const float* cost_host, int L,
                                   int32_t* labels_host) {
+  DeviceGuard dg(h);
   if (!h) return HGF_ERR_INVALID_ARGUMENT;
   h->launches = 0;
   h->err.clear();
@@ -950,6 +983,7 @@ hgf_status hgf_set_profiling(hgf_handle h, int enable) {
 }
 
 hgf_status hgf_profile_read(hgf_handle h, double* ms, int* counts, int n) {
+  DeviceGuard dg(h);
   if (!h || n < 0 || n > HGF_KC_COUNT) return HGF_ERR_INVALID_ARGUMENT;
   cudaError_t e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "profile sync");

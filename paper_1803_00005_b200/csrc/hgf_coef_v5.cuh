@@ -335,13 +335,17 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
   // band count minimising waves x (BH + 2R), waves = ceil(CTAs / 148), among band counts giving >= 8 waves
   // (or, for small images, the most CTAs) -- the same wave model as k_coef3.
   const int strips = (W + TX - 1) / TX, batches = (L + LB - 1) / LB;
-  int BH = H;
+  constexpr int kMaxBand = 320;
+  int BH = H < kMaxBand ? H : kMaxBand;
   {
     long long best = -1;
     const int nbmax = H / 32 > 1 ? H / 32 : 1;
+    // bands of at most kMaxBand rows: the fp32 running window sums are never restarted inside a band, so
+    // their rounding drift grows with the band length (parity at 270 rows: tests/test_gpu_parity.py)
+    const int nbmin = (H + kMaxBand - 1) / kMaxBand;
     const long long most = (long long)strips * ((H + (H + nbmax - 1) / nbmax - 1) / ((H + nbmax - 1) / nbmax)) * batches;
     const long long target = most < 8 * 148 ? most : 8 * 148;
-    for (int nb = 1; nb <= nbmax; ++nb) {
+    for (int nb = nbmin; nb <= (nbmax > nbmin ? nbmax : nbmin); ++nb) {
       const int bh = (H + nb - 1) / nb;
       const long long ctas = (long long)strips * ((H + bh - 1) / bh) * batches;
       if (ctas < target) continue;

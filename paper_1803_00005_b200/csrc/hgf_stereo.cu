@@ -190,7 +190,10 @@ cudaError_t launch_stereo_cost(const float* base, const float* other, const floa
                                int W, int H, int d0, int Lc, int dir, float a, float tc, float tg, cudaStream_t st) {
   if (Lc < 1) return cudaSuccess;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  if (W % 4 == 0 && Lc <= 4096 && al16(base) && al16(gb) && al16(cost)) {
+  // k_stereo_cost4 indexes columns x0 -+ d0 -+ Lc in 32-bit int: only when d0 + Lc stays within W + 2 segments
+  // (larger disparities all read as out of range, which the generic kernel handles in 64-bit arithmetic)
+  if (W % 4 == 0 && Lc <= 4096 && (long long)d0 + Lc <= (long long)W + 2 * SEG4 && al16(base) && al16(gb) &&
+      al16(cost)) {
     const size_t smem4 = sizeof(float) * 4 * (size_t)(SEG4 + Lc + 3);
     if (smem4 <= 200 * 1024) {
       auto kern = dir > 0 ? k_stereo_cost4<1> : k_stereo_cost4<-1>;
