@@ -261,7 +261,7 @@ HGF_API int hgf_last_launch_count(hgf_handle h);
 
 /* The slice-kernel pair this handle runs, fixed at create time from (W, H, n_guide, poly_degree, radius)
  * and the HGF_* selection variables: "coef5+agg3" (default for m <= 3, d <= 3, n <= 6, r <= 9, W % 4 == 0),
- * "coef3+agg3", "coef4+agg3", "coef2+agg3", "coef2+agg2", "coef1+agg1".  Static string; NULL handle -> "". */
+ * "coef5+agg5" (opt-in), "coef3+agg3", "coef4+agg3", "coef2+agg3", "coef2+agg2", "coef1+agg1".  Static string; NULL handle -> "". */
 HGF_API const char* hgf_kernel_path(hgf_handle h);
 
 /* Static description of a status code. */

@@ -53,6 +53,10 @@ struct hgf_ctx {
   bool v4coef = false;         // tensor-core coefficient kernel (planar layout for k_agg3, n <= 6, r <= 9)
   bool v5coef = false;         // horizontal-first coefficient kernel (interleaved layout, n <= 6, r <= 9): default
   CUtensorMap tm_g5;           // TMA descriptor over the raw guide planes of G for k_coef5 (box 164 x 1 x m)
+  bool v5agg = false;          // row-marching aggregation k_agg5 (default after k_coef5, n <= 6, r <= 9)
+  CUtensorMap tm_w5;           // k_agg5: rank-5 map over wbuf, box (16, 4, 6, 1, n + 1), 64-byte swizzle
+  CUtensorMap tm_ga5;          // k_agg5: map over G (W, H, n), box (64, 1, n)
+  int64_t* fkeys = nullptr;    // k_agg5: the frame's per-pixel minimum keys [H][W] (signed order, hgf.h)
   CUtensorMap tm_g4;           // TMA descriptor over G for k_coef4 (box kCoef4BoxX x 1 x n)
   CUtensorMap tm_g;            // TMA descriptor over G (dims W, H, n; box 88 x 1 x n) for k_coef3
   std::string err;
@@ -140,6 +144,7 @@ void release(hgf_ctx* h) {
   h->pool.clear();
   cudaFree(h->G);
   cudaFree(h->Gp);
+  cudaFree(h->fkeys);
   cudaFree(h->stats);
   cudaFree(h->wbuf);
   cudaFree(h->best_cost);
@@ -270,6 +275,10 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
 
 cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
   return traced(h, HGF_KC_AGG, h->stream, [&] {
+    if (h->v5agg)
+      return hgf::launch_agg_v5(h->n, &h->tm_w5, &h->tm_ga5, h->W, h->H, h->r, a.L, a.label_base,
+                                hgf::kWGroupLabels, reinterpret_cast<unsigned long long*>(h->fkeys), a.filtered_out,
+                                h->stream);
     if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, h->tm_w, a, h->stream);
     return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
   });
@@ -333,6 +342,12 @@ template <class BuildChunk>
 hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
                        int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out, BuildChunk build_chunk) {
   const long long HW = (long long)h->W * h->H;
+  if (h->v5agg && do_wta) {
+    // k_agg5 merges every CTA's band minima into the frame's key buffer: start from the MIN identity
+    cudaError_t e = traced(h, HGF_KC_KEYS, h->stream,
+                           [&] { return hgf::launch_fill_i64(h->fkeys, HW, 0x7fffffffffffffffLL, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(h, e, "keys fill");
+  }
   // balanced chunks (e.g. 256 labels with a 147-label capacity -> 2 x 128, not 128 + 128 + ... tails)
   const int nchunks = (L + h->lcap - 1) / h->lcap;
   int step = (L + nchunks - 1) / nchunks;
@@ -363,6 +378,13 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
     a.rows_per_owner = h->rows_per_owner;
     e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
+  }
+  if (h->v5agg && do_wta && (labels_out || min_cost_out || keys_out || h->peer_keys)) {
+    cudaError_t e = traced(h, HGF_KC_KEYS, h->stream, [&] {
+      return hgf::launch_keys_finalize(h->fkeys, h->W, h->H, labels_out, min_cost_out, keys_out, h->peer_keys,
+                                       h->rows_per_owner, h->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(h, e, "keys finalize");
   }
   return HGF_OK;
 }
@@ -395,6 +417,7 @@ int hgf_last_launch_count(hgf_handle h) { return h ? h->launches : 0; }
 const char* hgf_kernel_path(hgf_handle h) {
   if (!h) return "";
   if (h->v3agg) {
+    if (h->v5agg) return "coef5+agg5";
     if (h->v5coef) return "coef5+agg3";
     if (h->v4coef) return "coef4+agg3";
     if (h->v3coef) return "coef3+agg3";
@@ -503,6 +526,30 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->v4coef = false;
     h->v5coef = false;
     h->wlay = flat;
+  }
+  {
+    // k_agg5 (opt-in, HGF_AGG5=1: parity-green but slower than k_agg3 at C4 -- 32 vs 19 ms)
+    const char* f = std::getenv("HGF_AGG5");
+    h->v5agg = h->v5coef && h->v3agg && h->n <= hgf::kAgg5MaxN && h->r <= 9 && (f && f[0] == '1');
+    if (h->v5agg) {
+      auto encode = tensor_map_encoder();
+      const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
+      const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)H,
+                                  (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * K};
+      const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * H};
+      const cuuint32_t box[5] = {(cuuint32_t)G, (cuuint32_t)hgf::kAgg5LB, 6, 1, (cuuint32_t)K};
+      const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+      h->v5agg = encode &&
+                 encode(&h->tm_w5, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+                 encode_map_3d(&h->tm_ga5, h->G, W, H, h->n, W, (long long)W * H, 64, 1, h->n);
+      if (h->v5agg && cudaMalloc(&h->fkeys, sizeof(int64_t) * HW) != cudaSuccess) {
+        cudaGetLastError();
+        h->fkeys = nullptr;
+        h->v5agg = false;
+      }
+    }
   }
   *out = h;
   return HGF_OK;
@@ -943,7 +990,11 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
   if ((s = frame_stats(h, h->st_guide, 0, h->H)) != HGF_OK) return s;
   const long long lcap = h->st_chunk;
   const int nchunks = (int)((L + lcap - 1) / lcap);
-  const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+  if (h->v5agg) {
+    e = traced(h, HGF_KC_KEYS, h->stream,
+               [&] { return hgf::launch_fill_i64(h->fkeys, (long long)HW, 0x7fffffffffffffffLL, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(h, e, "keys fill");
+  }
   // double-buffered: copy chunk c+1 on copy_stream while chunk c is aggregated on the handle's stream
   for (int c = 0; c < nchunks; ++c) {
     const int b = c & 1;
@@ -968,6 +1019,12 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
     e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
     if ((e = cudaEventRecord(h->ev_used[b], h->stream)) != cudaSuccess) return cuda_fail(h, e, "record used");
+  }
+  if (h->v5agg) {
+    e = traced(h, HGF_KC_KEYS, h->stream, [&] {
+      return hgf::launch_keys_finalize(h->fkeys, h->W, h->H, h->st_labels, nullptr, nullptr, nullptr, 0, h->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(h, e, "keys finalize");
   }
   if ((e = cudaMemcpyAsync(labels_host, h->st_labels, sizeof(int32_t) * HW, cudaMemcpyDeviceToHost, h->stream)) !=
       cudaSuccess)

@@ -37,6 +37,26 @@ __global__ void k_unpack_keys(const int64_t* __restrict__ keys, int32_t* __restr
   }
 }
 
+// Final WTA outputs from the merged per-pixel keys (k_agg5 path): labels / min cost / keys, and the fused
+// label-sharded merge into the row owners' key buffers (system scope: several GPUs' atomics meet there).
+__global__ void k_keys_finalize(const int64_t* __restrict__ keys, int W, long long HW, int32_t* __restrict__ labels,
+                                float* __restrict__ cost, int64_t* __restrict__ keys_out,
+                                long long* const* __restrict__ peer_keys, int rows_per_owner) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
+    const int64_t ks = keys[p];
+    const uint64_t k = (uint64_t)ks ^ 0x8000000000000000ull;
+    if (labels) labels[p] = (int32_t)(uint32_t)(k & 0xffffffffull);
+    if (cost) cost[p] = from_orderable_bits((uint32_t)(k >> 32));
+    if (keys_out) keys_out[p] = ks;
+    if (peer_keys) {
+      const int y = (int)(p / W), x = (int)(p - (long long)y * W);
+      const int owner = y / rows_per_owner;
+      atomicMin_system(peer_keys[owner] + (long long)(y - owner * rows_per_owner) * W + x, (long long)ks);
+    }
+  }
+  if (peer_keys) __threadfence_system();
+}
+
 __global__ void k_fill_i64(int64_t* __restrict__ p, long long n, long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
@@ -46,6 +66,14 @@ __global__ void k_fill_i64(int64_t* __restrict__ p, long long n, long long v) {
 static int grid_1d(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   return (int)(b < 148LL * 32 ? (b < 1 ? 1 : b) : 148LL * 32);
+}
+
+cudaError_t launch_keys_finalize(const int64_t* keys, int W, int H, int32_t* labels_out, float* min_cost_out,
+                                 int64_t* keys_out, long long* const* peer_keys, int rows_per_owner, cudaStream_t st) {
+  const long long HW = (long long)W * H;
+  k_keys_finalize<<<grid_1d(HW, 256), 256, 0, st>>>(keys, W, HW, labels_out, min_cost_out, keys_out, peer_keys,
+                                                    rows_per_owner);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int m, int d, int W, int H, cudaStream_t st) {

@@ -131,6 +131,18 @@ cudaError_t launch_coef_v4(int n, const void* tm_vol, const void* tm_g, const fl
 // tm_vol: box kCoef5BoxX x 1 x kCoef5LB over the chunk's slices; tm_i: box kCoef5BoxX x 1 x m over the raw
 // guide channels (the planes G_{(i-1)d+1} = I_i of the guidance buffer).
 constexpr int kCoef5BoxX = 164, kCoef5LB = 32, kCoef5MaxN = 6;
+// Row-marching aggregation (hgf_agg_v5.cuh, instantiated in hgf_agg5.cu): n <= 6, r <= 9, the label-interleaved
+// layout.  tm_w: rank-5 map over the coefficient buffer (16 px, 32 labels, x groups, H, planes), box
+// (16, kAgg5LB, 6, 1, n + 1), 64-byte swizzle; tm_g: over G (W, H, n), box (64, 1, n).  Each CTA marches a band
+// for labels_per_cta labels (a multiple of kAgg5LB dividing 32) of the chunk's L and atomic-MINs the band's
+// minimum keys (signed order, hgf.h) into keys[H][W]; filtered_out (nullable) = the chunk's Z slices.
+constexpr int kAgg5LB = 4, kAgg5MaxN = 6;
+cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int H, int r, int L, int label_base,
+                          int labels_per_cta, unsigned long long* keys, float* filtered_out, cudaStream_t st);
+// keys[H][W] -> labels_out / min_cost_out / keys_out (each nullable) and, when peer_keys != null, a system-scope
+// 64-bit atomic MIN of every pixel's key into the row owner's buffer (the fused label-sharded merge).
+cudaError_t launch_keys_finalize(const int64_t* keys, int W, int H, int32_t* labels_out, float* min_cost_out,
+                                 int64_t* keys_out, long long* const* peer_keys, int rows_per_owner, cudaStream_t st);
 bool coef5_ok(int m, int d, int r);
 cudaError_t launch_coef_v5(int m, int d, const void* tm_vol, const void* tm_i, const float* stats, float* wbuf,
                            WLayout wo, int W, int H, int r, int L, cudaStream_t st);

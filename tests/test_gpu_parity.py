@@ -467,6 +467,9 @@ BAND_CASES = [
     # (name, W, H, L, distribution, env, expected kernel path)
     ("coef5-3strips-3bands-2batches", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
     ("coef5-iid-band270", 260, 560, 34, "iid", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
+    # the opt-in row-marching aggregation (k_agg5) at its band length: 3 bands x 2 label groups
+    ("coef5-agg5", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270", "HGF_AGG5": "1", "HGF_AGG5_BH": "270"},
+     "coef5+agg5"),
     ("coef3-band270", 300, 560, 40, "stereo", {"HGF_COEF5": "0", "HGF_COEF3_BH": "270"}, "coef3+agg3"),
 ]
 
