@@ -38,14 +38,17 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=64)
-    ap.add_argument("--cpu-sample-labels", type=int, default=32)
+    ap.add_argument("--cpu-sample-labels", type=int, default=8, help="labels per host core in the CPU baseline")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- algorithmic work
 def alg_flops_per_voxel(n):
-    """Per voxel (fp32), as counted in DESIGN.md §5: coef 2n^2+9n+5, agg 6n+6."""
-    return {"coef": 2 * n * n + 9 * n + 5, "agg": 6 * n + 6}
+    """Per voxel (fp32): F(n) = 2n^2 + 17n + 13, split by kernel class --
+    coef (steps A5 + A6): n products + 4(n+1) stage-1 box adds + (1 + 2n) for m_p and c' + (2n^2 + 2n) matvec
+    and h + (2n + 2) w_0 = 2n^2 + 11n + 7 (145 at n = 6); agg (A7 + A8): 4(n+1) stage-2 box adds + (2n + 1) Z
+    + 1 WTA = 6n + 6 (42 at n = 6)."""
+    return {"coef": 2 * n * n + 11 * n + 7, "agg": 6 * n + 6}
 
 
 def alg_flops_stats_per_pixel(n):
@@ -140,16 +143,59 @@ def make_band(scene, c, y0, rows, labels):
     return sub.left, V, y0 - ya
 
 
-def cpu_baseline(scene, c, rows, labels, y0=None):
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_labels_worker(job):
+    """One process of the label-parallel CPU baseline: the oracle on a label sub-range of the band."""
+    import numpy as np
+
+    import oracle as O
+    I, V, lam, r, d = job
+    Z = O.hgf_filter(I, V, lam, r, d)
+    return Z.min(axis=0), np.argmin(Z, axis=0)
+
+
+def cpu_baseline(scene, c, rows, labels_per_core, y0=None):
+    """The float64 oracle (as it stands) on a bounded sample of the workload, label-parallel over every host core
+    the process may use: one process per core, OPENBLAS_NUM_THREADS=1, labels split contiguously,
+    per-pixel minima merged; wall time of the whole sample."""
+    import multiprocessing as mp
+
+    import numpy as np
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     y0 = c["H"] // 2 if y0 is None else y0
     rows = min(rows, c["H"])
     y0 = min(y0, c["H"] - rows)
-    labels = min(labels, c["L"])
+    labels = min(c["L"], labels_per_core * cores)
     I, V, halo = make_band(scene, c, y0, rows, labels)
-    vox, dt = oracle_sample(I, V, c, y0, rows, halo)
-    return {"value": vox / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    bounds = np.linspace(0, labels, min(cores, labels) + 1).astype(int)
+    jobs = [(I, np.ascontiguousarray(V[a:b]), c["lam"], c["r"], c["d"]) for a, b in zip(bounds[:-1], bounds[1:])
+            if b > a]
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("fork")
+    t = time.perf_counter()
+    with ctx.Pool(len(jobs)) as pool:
+        parts = pool.map(_oracle_labels_worker, jobs)
+    best = np.full(parts[0][0].shape, np.inf)
+    lab = np.zeros(parts[0][0].shape, dtype=np.int64)
+    for (mn, am), a in zip(parts, bounds[:-1]):
+        upd = mn < best
+        best = np.where(upd, mn, best)
+        lab = np.where(upd, am + a, lab)
+    dt = time.perf_counter() - t
+    vox = rows * c["W"] * labels
+    return {"value": vox / dt, "unit": UNIT, "cores": len(jobs), "kind": "oracle",
             "sample": (f"rows {y0}-{y0 + rows - 1} (+{2 * c['r']}-row halos) x {c['W']} cols x labels 0-{labels - 1} "
-                       f"of {c['name']}: {vox} voxels in {dt:.2f} s, numpy float64, 1 thread")}
+                       f"of {c['name']}: {vox} voxels in {dt:.2f} s wall, numpy float64, label-parallel over "
+                       f"{len(jobs)} processes x 1 thread ({cores} cores available; CPU: {_cpu_model()})")}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -420,18 +466,25 @@ def main():
         flops_total = alg_flops_stats_per_pixel(n) * W * H * args.steps
         peak = SM_COUNT * FP64_LANES * 2 * 1965e6 / 1e12
     achieved = flops_total / dom_cnt / (dom_ms / dom_cnt / 1e3) / 1e12 if dom_cnt else 0.0
-    traffic = None
+    # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the `ncu --set full`
+    # capture committed in profiles/ncu_traffic.json -- used only when it was taken of the kernel this handle runs
+    # (the file names the kernel and the commit it was captured at)
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
             ent = tj.get(c["name"], {}).get(dom)
-            if ent is not None:
-                traffic = ent
+            path_kernels = {"coef": h.kernel_path.split("+")[0], "agg": h.kernel_path.split("+")[1]}
+            if isinstance(ent, dict) and (dom == "stats" or ent.get("kernel", "").startswith("k_" + path_kernels[dom])):
+                traffic = ent["bytes_per_launch"]
+                traffic_src = f"{ent['kernel']} @ {tj.get('_commit', '?')} ({ent.get('labels_per_launch')} labels/launch)"
         except Exception:
             traffic = None
     roofline = {"bound": "alu", "kernel": {"coef": "k_coef", "agg": "k_agg", "stats": "k_stats"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": traffic_src, "kernels": h.kernel_path,
+                "flops_per_voxel": fl[dom] if dom in ("coef", "agg") else None,
                 "peak_basis": ("148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts/clock)"
                                if dom != "stats" else "148 SMs x 64 FP64 lanes x 2 x 1965 MHz"),
                 "share_of_step": dom_ms / (ms_max if world == 1 else ms) if ms else None}
