@@ -179,9 +179,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
   extern __shared__ __align__(128) float sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NST * Gm::STAGE);   // full barriers (TMA tx count)
   const int tid = threadIdx.x, lane = tid & 31, seg = tid >> 5;
-  const int x0 = blockIdx.x * TX;
-  const int Y0 = blockIdx.y * BH, Y1 = min(H, Y0 + BH);
-  const int lb0 = blockIdx.z * LB;
+  // grid (label batches, strips, bands): the batches of one (strip, band) are adjacent in launch order, so they
+  // run at the same time and share each guidance row and statistics row through L2
+  const int x0 = blockIdx.y * TX;
+  const int Y0 = blockIdx.z * BH, Y1 = min(H, Y0 + BH);
+  const int lb0 = blockIdx.x * LB;
   const int xt = x0 - R - SH;                       // TMA x start (16-byte aligned: x0 % 4 == 0)
   const int nsteps = 2 * R + (Y1 - Y0);             // entering rows Y0 - R .. Y1 - 1 + R
   const int nx = min(TX, W - x0);                   // pixels of the strip inside the image
@@ -355,7 +357,7 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
   }
   static const int bh_env = std::getenv("HGF_COEF5_BH") ? std::atoi(std::getenv("HGF_COEF5_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning / test runs only
-  dim3 grid(strips, (H + BH - 1) / BH, batches);
+  dim3 grid(batches, strips, (H + BH - 1) / BH);
   k_coef5<M, D, R><<<grid, NW * 32, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),
                                                     *reinterpret_cast<const CUtensorMap*>(tm_i), stats, wbuf, wo, W, H,
                                                     L, BH);
