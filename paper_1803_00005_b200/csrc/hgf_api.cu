@@ -21,7 +21,9 @@ struct hgf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   float* G = nullptr;          // [n][H][W]     polynomial guidance (K1)
-  float* Gp = nullptr;         // [H][m][W][2]  (I_i, I_i^2) pairs for k_coef5 when d = 2 (K1)
+  float* Gp = nullptr;         // [H][m][gp_pitch][2]  (I_i, I_i^2) pairs for k_coef5 when d = 2 (K1)
+  int gp_pitch = 0;            // Gp row pitch in pairs (W rounded up to even)
+  float* vpad = nullptr;       // W % 4 != 0: one chunk of the cost volume in rows of ceil4(W) floats (k_coef5 TMA)
   float* stats = nullptr;      // [NS][H][W]    P' upper triangle + nu (K3)
   float* wbuf = nullptr;       // [lcap][n+1][H][W] per-slice coefficients w (K4a -> K4b)
   int lcap = 0;                // labels per coefficient chunk
@@ -144,6 +146,7 @@ void release(hgf_ctx* h) {
   h->pool.clear();
   cudaFree(h->G);
   cudaFree(h->Gp);
+  cudaFree(h->vpad);
   cudaFree(h->fkeys);
   cudaFree(h->stats);
   cudaFree(h->wbuf);
@@ -181,7 +184,7 @@ hgf_status check_async(hgf_ctx* h) {
 // Steps 1-2: polynomial guidance (all rows) and the statistics of rows [y0, y1).
 hgf_status frame_stats(hgf_ctx* h, const float* guide, int y0, int y1) {
   cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
-    return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->m, h->d, h->W, h->H, h->stream);
+    return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->gp_pitch, h->m, h->d, h->W, h->H, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
@@ -249,10 +252,24 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
                                  h->stream);
     }
     if (h->v5coef) {
-      // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 164 x 1 x 32 (k_coef5)
+      // TMA descriptor over this chunk's cost slices: dims (W, H, Lc), box 164 x 1 x 32 (k_coef5); rows must be
+      // 16-byte multiples, so for W % 4 != 0 the chunk is first copied into rows of ceil4(W) floats (the TMA
+      // still reads columns >= W as zero: the tensor's x extent stays W)
+      long long pitch = h->W;
+      if (h->W % 4) {
+        pitch = (h->W + 3) / 4 * 4;
+        if (!h->vpad) {
+          cudaError_t e = cudaMalloc(&h->vpad, sizeof(float) * (size_t)h->lcap * h->H * pitch);
+          if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaMemcpy2DAsync(h->vpad, sizeof(float) * pitch, vol_chunk, sizeof(float) * h->W,
+                                          sizeof(float) * h->W, (size_t)h->H * Lc, cudaMemcpyDeviceToDevice, h->stream);
+        if (e != cudaSuccess) return e;
+        vol_chunk = h->vpad;
+      }
       CUtensorMap tm_vol;
-      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, hgf::kCoef5BoxX,
-                         1, hgf::kCoef5LB))
+      if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, pitch, pitch * h->H, hgf::kCoef5BoxX, 1,
+                         hgf::kCoef5LB))
         return cudaErrorInvalidValue;
       return hgf::launch_coef_v5(h->m, h->d, &tm_vol, &h->tm_g5, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc,
                                  h->stream);
@@ -469,14 +486,19 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     const char* f5 = std::getenv("HGF_COEF5");
     // tm_g5: d = 2: the (I_i, I_i^2) pairs [H][m][W] as 8-byte elements, dims (W, m, H); other degrees: the raw
     // guide channels I_i = G_{(i-1)d+1} (every d-th plane of the guidance buffer), dims (W, H, m)
-    h->v5coef = h->v3coef && hgf::coef5_ok(h->m, h->d, h->r) && !(f5 && f5[0] == '0');
+    // W % 4 != 0 (the paper's 450-column Middlebury frames, BASELINE config 2): each chunk of the cost volume is
+    // first copied into a pitched scratch (rows of ceil4(W) floats, the TMA stride rule) -- degree 2 only, whose
+    // guide pairs have their own pitched buffer
+    h->v5coef = h->v3agg && !h->v4coef && hgf::coef5_ok(h->m, h->d, h->r) && !(f5 && f5[0] == '0') &&
+                !(f && f[0] == '0') && ((W % 4) == 0 || h->d == 2);
+    h->gp_pitch = W + (W & 1);                 // guide pairs: 8-byte elements, rows of 16-byte multiples
     if (h->v5coef && h->d == 2) {
-      if (cudaMalloc(&h->Gp, sizeof(float) * 2 * h->m * HW) != cudaSuccess) {
+      if (cudaMalloc(&h->Gp, sizeof(float) * 2 * h->m * (size_t)h->gp_pitch * H) != cudaSuccess) {
         cudaGetLastError();
         h->Gp = nullptr;
       }
-      h->v5coef = h->Gp && encode_map_3d_u64(&h->tm_g5, h->Gp, W, h->m, H, W, (long long)W * h->m, hgf::kCoef5BoxX,
-                                             h->m, 1);
+      h->v5coef = h->Gp && encode_map_3d_u64(&h->tm_g5, h->Gp, W, h->m, H, h->gp_pitch, (long long)h->gp_pitch * h->m,
+                                             hgf::kCoef5BoxX, h->m, 1);
     } else if (h->v5coef) {
       h->v5coef = encode_map_3d(&h->tm_g5, h->G, W, H, h->m, W, (long long)W * H * h->d, hgf::kCoef5BoxX, 1, h->m);
     }
@@ -497,7 +519,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   hgf::WLayout lines = padded;          // k_coef4: rows start on 128-byte lines (one line per warp store)
   lines.pitch = (W + 31) / 32 * 32;
   lines.plane = (long long)H * lines.pitch;
-  h->wlay = h->v3coef ? inter : (h->v4coef ? lines : (h->v3agg ? padded : flat));
+  h->wlay = (h->v3coef || h->v5coef) ? inter : (h->v4coef ? lines : (h->v3agg ? padded : flat));
   const size_t per_label = (size_t)K * (size_t)h->wlay.plane * sizeof(float);
   size_t cap = coef_budget_bytes() / per_label;
   cap = cap < 1 ? 1 : (cap > 4096 ? 4096 : cap);
@@ -614,7 +636,7 @@ hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1) {
   h->err.clear();
   if (!guide) return fail(h, HGF_ERR_INVALID_ARGUMENT, "null guide");
   if (y0 < 0 || y1 > h->H || y0 > y1) return fail(h, HGF_ERR_INVALID_ARGUMENT, "row band out of range");
-  if (!(h->v3coef || h->v4coef))
+  if (!(h->v3coef || h->v4coef || h->v5coef))
     return fail(h, HGF_ERR_UNSUPPORTED, "row-band statistics need the per-pixel statistics layout (n <= 6, W % 4 == 0)");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
@@ -624,7 +646,7 @@ hgf_status hgf_prepare_rows(hgf_handle h, const float* guide, int y0, int y1) {
 hgf_status hgf_stats_buffer(hgf_handle h, void** dev_ptr, size_t* bytes_per_row) {
   DeviceGuard dg(h);
   if (!h || !dev_ptr || !bytes_per_row) return HGF_ERR_INVALID_ARGUMENT;
-  if (!(h->v3coef || h->v4coef))
+  if (!(h->v3coef || h->v4coef || h->v5coef))
     return fail(h, HGF_ERR_UNSUPPORTED, "statistics are not stored row-contiguously in this configuration");
   *dev_ptr = h->stats;
   *bytes_per_row = sizeof(float) * (size_t)hgf::stats_aos_floats(h->n) * h->W;
@@ -644,7 +666,8 @@ hgf_status hgf_aggregate_wta_prepared(hgf_handle h, const float* cost_volume, in
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
   if (!labels_out && !min_cost_out && !filtered_out && !keys_out)
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
-  if (!(h->v3coef || h->v4coef)) return fail(h, HGF_ERR_UNSUPPORTED, "prepared statistics need the k_coef3/4 path");
+  if (!(h->v3coef || h->v4coef || h->v5coef))
+    return fail(h, HGF_ERR_UNSUPPORTED, "prepared statistics need the k_coef3/4/5 path");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
@@ -865,8 +888,8 @@ hgf_status hgf_aggregate_wta_peer(hgf_handle h, const float* cost_volume, int L,
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "label_offset out of range");
   if (world < 1 || rows_per_owner < 1 || (long long)rows_per_owner * world < h->H)
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "owners must cover every row: world * rows_per_owner >= H");
-  if (!h->v3agg || !(h->v3coef || h->v4coef))
-    return fail(h, HGF_ERR_UNSUPPORTED, "the fused merge needs the k_coef3/4 + k_agg3 path");
+  if (!h->v3agg || !(h->v3coef || h->v4coef || h->v5coef))
+    return fail(h, HGF_ERR_UNSUPPORTED, "the fused merge needs the k_coef3/4/5 + k_agg3 path");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   h->peer_keys = reinterpret_cast<long long* const*>(peer_keys_dev);

@@ -8,9 +8,9 @@
 namespace hgf {
 
 // ------------------------------------------------------------------ K1: polynomial guidance
-// Gp (optional, d = 2): the same powers as (I_i, I_i^2) pairs, layout [H][m][W][2] (k_coef5's guide rows).
-__global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__ G, float2* __restrict__ Gp, int m, int d,
-                                int W, long long HW) {
+// Gp (optional, d = 2): the same powers as (I_i, I_i^2) pairs, layout [H][m][gp][2] (k_coef5's guide rows).
+__global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__ G, float2* __restrict__ Gp, int gp, int m,
+                                int d, int W, long long HW) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < HW; p += (long long)gridDim.x * blockDim.x) {
     for (int i = 0; i < m; ++i) {
       const float v = I[i * HW + p];
@@ -22,7 +22,7 @@ __global__ void k_poly_guidance(const float* __restrict__ I, float* __restrict__
       }
       if (Gp) {
         const long long y = p / W, x = p - y * W;
-        Gp[(y * m + i) * W + x] = make_float2(v, v * v);
+        Gp[(y * m + i) * gp + x] = make_float2(v, v * v);
       }
     }
   }
@@ -76,10 +76,11 @@ cudaError_t launch_keys_finalize(const int64_t* keys, int W, int H, int32_t* lab
   return cudaGetLastError();
 }
 
-cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int m, int d, int W, int H, cudaStream_t st) {
+cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int gp_pitch, int m, int d, int W, int H,
+                                 cudaStream_t st) {
   const long long HW = (long long)W * H;
-  k_poly_guidance<<<grid_1d(HW, 256), 256, 0, st>>>(I, G, reinterpret_cast<float2*>(d == 2 ? Gp : nullptr), m, d, W,
-                                                      HW);
+  k_poly_guidance<<<grid_1d(HW, 256), 256, 0, st>>>(I, G, reinterpret_cast<float2*>(d == 2 ? Gp : nullptr), gp_pitch,
+                                                      m, d, W, HW);
   return cudaGetLastError();
 }
 

@@ -27,8 +27,9 @@ struct AggArgs {
   int rows_per_owner;
 };
 
-// Gp (nullable; used when d == 2): (I_i, I_i^2) pairs, layout [H][m][W][2], for k_coef5.
-cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int m, int d, int W, int H, cudaStream_t st);
+// Gp (nullable; used when d == 2): (I_i, I_i^2) pairs, layout [H][m][gp_pitch][2], for k_coef5.
+cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int gp_pitch, int m, int d, int W, int H,
+                                 cudaStream_t st);
 // aos = 1: per-pixel records of kStatsAos floats (statistics, then kappa = 1/(lam0f + N)) for k_coef3;
 // needs the k_stats2 path (else cudaErrorInvalidValue).
 // Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).

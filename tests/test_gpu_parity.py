@@ -89,8 +89,12 @@ def test_aggregate_parity(name, W, H, m, d, L, r, lam, mode):
 
 
 def test_c2_full_parity():
-    """BASELINE config 2 in full: 450x375 Middlebury size, degree-2 RGB (n = 6), 60 labels, r = 9."""
+    """BASELINE config 2 in full: 450x375 Middlebury size, degree-2 RGB (n = 6), 60 labels, r = 9 -- on the
+    default k_coef5 -> k_agg3 path (W % 4 != 0: each chunk is repacked into 452-float rows for the TMA)."""
     c = synth.config("C2")
+    h = _hgf(c["W"], c["H"], c["m"], c["d"], c["r"], c["lam"])
+    assert h.kernel_path == "coef5+agg3", h.kernel_path
+    h.close()
     scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
     V = synth.stereo_cost_volume_np(scene, c["L"])
     res = _run(scene.left, V, c["d"], c["r"], c["lam"])
@@ -244,7 +248,8 @@ def test_prepared_row_bands_equal_unsharded(monkeypatch, coef4):
 def test_prepared_path_unsupported_config_fails_loudly():
     torch = _torch()
     from paper_1803_00005_b200 import HGFError
-    h = _hgf(42, 30, 3, 2, 4, 0.05, "hgf")                  # W % 4 != 0: planar statistics, no row bands
+    h = _hgf(42, 30, 3, 3, 4, 0.05, "hgf")                  # W % 4 != 0, degree 3: planar statistics, no row bands
+    assert h.kernel_path == "coef2+agg3"
     with pytest.raises(HGFError):
         h.prepare_rows(torch.zeros(3, 30, 42, device="cuda"), 0, 30)
     with pytest.raises(HGFError):
@@ -471,6 +476,8 @@ BAND_CASES = [
     ("coef5-agg5", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270", "HGF_AGG5": "1", "HGF_AGG5_BH": "270"},
      "coef5+agg5"),
     ("coef3-band270", 300, 560, 40, "stereo", {"HGF_COEF5": "0", "HGF_COEF3_BH": "270"}, "coef3+agg3"),
+    # W % 4 != 0 on k_coef5 (repacked rows; odd width: the guide pairs' own pitch), 3 strips
+    ("coef5-odd-width", 301, 140, 40, "stereo", {}, "coef5+agg3"),
 ]
 
 
@@ -499,7 +506,7 @@ def test_full_frame_band_geometry(monkeypatch, name, W, H, L, dist, env, path):
 
 def test_default_kernel_path_is_coef5():
     """The headline configs (RGB degree 2, r = 9, W % 4 == 0) run k_coef5 -> k_agg3 by default."""
-    for W, H in ((3840, 2160), (1920, 1080), (452, 375)):
+    for W, H in ((3840, 2160), (1920, 1080), (452, 375), (450, 375), (451, 77)):
         h = _hgf(W, H, 3, 2, 9, 0.05)
         assert h.kernel_path == "coef5+agg3", (W, H, h.kernel_path)
         h.close()
