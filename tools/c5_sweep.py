@@ -18,7 +18,7 @@ rows = []
 for d, ms_ in ((1, (1, 2, 3, 4, 6, 8, 10, 12, 16, 20)), (2, (1, 2, 3, 4, 5, 6, 8, 10)), (3, (1, 2, 3, 4, 5, 6))):
     for m in ms_:
         I = torch.from_numpy(synth.smooth_guides(W, H, m, seed=5)).cuda()
-        for r in (4, 8, 12, 16):
+        for r in (4, 8, 9, 12, 16):
             h = HGF(W, H, m, d, r, 0.05)
             dst = torch.empty((H, W), dtype=torch.float32, device="cuda")
             for _ in range(3):
@@ -34,7 +34,9 @@ for d, ms_ in ((1, (1, 2, 3, 4, 6, 8, 10, 12, 16, 20)), (2, (1, 2, 3, 4, 5, 6, 8
             h.set_profiling(True)
             h.filter(I, Y, dst)
             prof = {k: round(v[0], 3) for k, v in h.profile_read().items() if v[1]}
+            path = h.kernel_path
             h.close()
             ts.sort()
-            rows.append({"m": m, "d": d, "n": m * d, "r": r, "ms": round(ts[2], 3), "stage_ms": prof})
+            rows.append({"m": m, "d": d, "n": m * d, "r": r, "ms": round(ts[2], 3), "stage_ms": prof,
+                         "kernels": path})
             print(json.dumps(rows[-1]), flush=True)
