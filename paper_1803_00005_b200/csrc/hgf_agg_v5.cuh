@@ -278,7 +278,7 @@ cudaError_t agg5_r(const void* tm_w, const void* tm_g, int W, int H, int L, int 
       if (best < 0 || cost < best) { best = cost; BH = bh; }
     }
   }
-  static const int bh_env = std::getenv("HGF_AGG5_BH") ? std::atoi(std::getenv("HGF_AGG5_BH")) : 0;
+  const int bh_env = std::getenv("HGF_AGG5_BH") ? std::atoi(std::getenv("HGF_AGG5_BH")) : 0;
   if (bh_env >= 8 && bh_env <= MAXBAND) BH = bh_env;
   dim3 grid(strips, (H + BH - 1) / BH, groups);
   k_agg5<NC, R><<<grid, THREADS, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_w),

@@ -50,6 +50,12 @@ struct hgf_ctx {
   bool fast = false;           // v2 fast-path kernels usable for (m, d, r)
   bool v3agg = false;          // TMA-fed v3 aggregation usable (n <= 9, r <= 9, W % 4 == 0)
   CUtensorMap tm_w[2];         // TMA descriptors over wbuf for k_agg3's two plane groups
+  // two-stream chunk pipeline (interleaved layout): the coefficient buffer as two halves of `half` labels; the
+  // coefficients of chunk c + 1 (handle stream) overlap the aggregation of chunk c (aux stream)
+  int half = 0;                // labels per half (multiple of 32), 0 = no pipeline
+  CUtensorMap tm_wh[2][2];     // k_agg3 maps over half b, plane groups A / B
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_coef[2] = {nullptr, nullptr}, ev_agg[2] = {nullptr, nullptr}, ev_join = nullptr;
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
   bool v4coef = false;         // tensor-core coefficient kernel (planar layout for k_agg3, n <= 6, r <= 9)
@@ -164,6 +170,12 @@ void release(hgf_ctx* h) {
   cudaFree(h->st_vol[1]);
   cudaFree(h->st_labels);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_coef[i]) cudaEventDestroy(h->ev_coef[i]);
+    if (h->ev_agg[i]) cudaEventDestroy(h->ev_agg[i]);
+  }
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
@@ -240,8 +252,9 @@ bool encode_map_3d_u64(CUtensorMap* tm, const void* base, long long dx, long lon
 }
 
 // K4a for one chunk of Lc slices: the v2 fast path when (m, d, r) allow it, else the generic v1 kernel.
-cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc) {
+cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_chunk, int Lc, float* wdst = nullptr) {
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+  if (!wdst) wdst = h->wbuf;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
     if (h->v4coef) {
       CUtensorMap tm_vol;
@@ -271,7 +284,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
       if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, pitch, pitch * h->H, hgf::kCoef5BoxX, 1,
                          hgf::kCoef5LB))
         return cudaErrorInvalidValue;
-      return hgf::launch_coef_v5(h->m, h->d, &tm_vol, &h->tm_g5, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc,
+      return hgf::launch_coef_v5(h->m, h->d, &tm_vol, &h->tm_g5, h->stats, wdst, h->wlay, h->W, h->H, h->r, Lc,
                                  h->stream);
     }
     if (h->v3coef) {
@@ -280,7 +293,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
       if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H, 88, 1,
                          hgf::coef3_labels(h->n)))
         return cudaErrorInvalidValue;
-      return hgf::launch_coef_v3(h->n, &tm_vol, &h->tm_g, h->stats, h->wbuf, h->wlay, h->W, h->H, h->r, Lc, lam0,
+      return hgf::launch_coef_v3(h->n, &tm_vol, &h->tm_g, h->stats, wdst, h->wlay, h->W, h->H, h->r, Lc, lam0,
                                  h->stream);
     }
     if (h->fast)
@@ -290,7 +303,13 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
   });
 }
 
-cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
+cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a, const void* tmaps = nullptr,
+                             cudaStream_t st = nullptr) {
+  if (!tmaps) tmaps = h->tm_w;
+  if (!st) st = h->stream;
+  if (st != h->stream) {
+    return traced(h, HGF_KC_AGG, st, [&] { return hgf::launch_agg_v3(h->n, h->r, tmaps, a, st); });
+  }
   return traced(h, HGF_KC_AGG, h->stream, [&] {
     if (h->v5agg)
       return hgf::launch_agg_v5(h->n, &h->tm_w5, &h->tm_ga5, h->W, h->H, h->r, a.L, a.label_base,
@@ -303,7 +322,10 @@ cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a) {
 
 // TMA descriptor over the coefficient buffer for the v3 aggregation kernel (driver entry point via the
 // runtime, so the library does not link libcuda directly).
-bool make_wbuf_tensor_map(hgf_ctx* h) {
+bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out);
+bool make_wbuf_tensor_map(hgf_ctx* h) { return make_wbuf_maps(h, h->wbuf, h->lcap, h->tm_w); }
+
+bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
@@ -330,21 +352,21 @@ bool make_wbuf_tensor_map(hgf_ctx* h) {
       // box = one label's planes of a BX x BY tile, 4G-byte inner runs, 64-byte swizzle (k_agg3's swz)
       const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
       const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
-                                  (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * K};
+                                  (cuuint64_t)(labels / hgf::kWGroupLabels) * K};
       const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * h->H};
       const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, planes};
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-      r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
+      r = encode(&out[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, base, dims, strides, box, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE,
                  hgf::kWGroupPx == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, wmap_l2_promotion(),
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
-                                  (cuuint64_t)h->lcap * K};
+                                  (cuuint64_t)labels * K};
       const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
       const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, planes};
       const cuuint32_t estr[3] = {1, 1, 1};
-      r = encode(&h->tm_w[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->wbuf, dims, strides, box, estr,
+      r = encode(&out[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
@@ -359,6 +381,69 @@ template <class BuildChunk>
 hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
                        int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out, BuildChunk build_chunk) {
   const long long HW = (long long)h->W * h->H;
+  // opt-in (HGF_PIPELINE=1): measured slower at C4 (36.3 vs 35.2 ms: the overlapped kernels slow each other down
+  // -- coef 14.8 -> 20.5 ms, agg 19.2 -> 27.3 ms of device time -- on top of 4 chunks' tails instead of 2)
+  const bool pipe_env = std::getenv("HGF_PIPELINE") && std::getenv("HGF_PIPELINE")[0] == '1';
+  if (h->half > 0 && !h->v5agg && L > h->half && pipe_env) {
+    // ---- two-stream chunk pipeline: chunk c's coefficients go to half c % 2 of the buffer on the handle's
+    // stream while chunk c - 1 is aggregated on the aux stream (the coefficient kernel is DRAM-bound, the
+    // aggregation shared-memory-bound: running them side by side overlaps the two limits)
+    cudaError_t e = cudaSuccess;
+    if (!h->aux) {
+      if ((e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(h, e, "aux stream");
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&h->ev_coef[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_agg[i], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(h, e, "pipeline events");
+    }
+    const int K = h->n + 1;
+    const long long half_floats =
+        (long long)(h->half / hgf::kWGroupLabels) * K * h->H * h->wlay.xg * (hgf::kWGroupPx * hgf::kWGroupLabels);
+    const int nchunks = (L + h->half - 1) / h->half;
+    int step = (L + nchunks - 1) / nchunks;
+    step = (step + hgf::kWGroupLabels - 1) / hgf::kWGroupLabels * hgf::kWGroupLabels;
+    if (step > h->half) step = h->half;
+    int ci = 0;
+    for (int c0 = 0; c0 < L; c0 += step, ++ci) {
+      const int Lc = (L - c0 < step) ? (L - c0) : step;
+      const int b = ci & 1;
+      const float* chunk = vol ? vol + (long long)c0 * HW : nullptr;
+      e = build_chunk(c0, Lc, &chunk);
+      if (e != cudaSuccess) return cuda_fail(h, e, "cost construction");
+      if (ci >= 2 && (e = cudaStreamWaitEvent(h->stream, h->ev_agg[b], 0)) != cudaSuccess)
+        return cuda_fail(h, e, "wait half free");
+      e = launch_coef_chunk(h, guide, chunk, Lc, h->wbuf + b * half_floats);
+      if (e != cudaSuccess) return cuda_fail(h, e, "coef");
+      if ((e = cudaEventRecord(h->ev_coef[b], h->stream)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(h->aux, h->ev_coef[b], 0)) != cudaSuccess)
+        return cuda_fail(h, e, "coef -> agg");
+      hgf::AggArgs a{};
+      a.G = h->G;
+      a.wbuf = h->wbuf + b * half_floats;
+      a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = h->wlay.pad; a.il = h->wlay.il;
+      a.label_base = label_offset + c0;
+      a.filtered_out = filtered_out ? filtered_out + (long long)c0 * HW : nullptr;
+      a.do_wta = do_wta;
+      a.first = (c0 == 0);
+      a.last = (c0 + Lc >= L);
+      a.best_cost = h->best_cost;
+      a.best_label = h->best_label;
+      a.labels_out = labels_out;
+      a.min_cost_out = min_cost_out;
+      a.keys_out = keys_out;
+      a.peer_keys = h->peer_keys;
+      a.rows_per_owner = h->rows_per_owner;
+      e = launch_agg_chunk(h, a, h->tm_wh[b], h->aux);
+      if (e != cudaSuccess) return cuda_fail(h, e, "agg");
+      if ((e = cudaEventRecord(h->ev_agg[b], h->aux)) != cudaSuccess) return cuda_fail(h, e, "record agg");
+    }
+    if ((e = cudaEventRecord(h->ev_join, h->aux)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(h->stream, h->ev_join, 0)) != cudaSuccess)
+      return cuda_fail(h, e, "join");
+    return HGF_OK;
+  }
   if (h->v5agg && do_wta) {
     // k_agg5 merges every CTA's band minima into the frame's key buffer: start from the MIN identity
     cudaError_t e = traced(h, HGF_KC_KEYS, h->stream,
@@ -548,6 +633,15 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->v4coef = false;
     h->v5coef = false;
     h->wlay = flat;
+  }
+  if (h->v3agg && h->wlay.il && h->lcap >= 2 * hgf::kWGroupLabels) {
+    // the two halves of the coefficient buffer for the two-stream chunk pipeline (slices_impl)
+    h->half = (h->lcap / 2) / hgf::kWGroupLabels * hgf::kWGroupLabels;
+    const long long half_floats =
+        (long long)(h->half / hgf::kWGroupLabels) * K * H * h->wlay.xg * (hgf::kWGroupPx * hgf::kWGroupLabels);
+    if (!(make_wbuf_maps(h, h->wbuf, h->half, h->tm_wh[0]) &&
+          make_wbuf_maps(h, h->wbuf + half_floats, h->half, h->tm_wh[1])))
+      h->half = 0;
   }
   {
     // k_agg5 (opt-in, HGF_AGG5=1: parity-green but slower than k_agg3 at C4 -- 32 vs 19 ms)

@@ -362,7 +362,7 @@ cudaError_t coef3_r(const void* tm_vol, const void* tm_g, const float* stats, fl
       if (best < 0 || cost < best) { best = cost; BH = bh; }
     }
   }
-  static const int bh_env = std::getenv("HGF_COEF3_BH") ? std::atoi(std::getenv("HGF_COEF3_BH")) : 0;
+  const int bh_env = std::getenv("HGF_COEF3_BH") ? std::atoi(std::getenv("HGF_COEF3_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning runs only
   dim3 grid(strips, (H + BH - 1) / BH, batches);
   k_coef3<NC, R><<<grid, Gm::THREADS, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),

@@ -355,7 +355,7 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
       if (best < 0 || cost < best) { best = cost; BH = bh; }
     }
   }
-  static const int bh_env = std::getenv("HGF_COEF5_BH") ? std::atoi(std::getenv("HGF_COEF5_BH")) : 0;
+  const int bh_env = std::getenv("HGF_COEF5_BH") ? std::atoi(std::getenv("HGF_COEF5_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning / test runs only
   dim3 grid(batches, strips, (H + BH - 1) / BH);
   k_coef5<M, D, R><<<grid, NW * 32, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),

@@ -104,7 +104,7 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
                        (size_t)7 * 16 * 16 * 8 + 16;
   // k_stats4 (row-marching Gram sums, hgf_stats_v4.cuh) for n <= kStats4MaxN; HGF_STATS2=1 keeps the
   // tiled k_stats2 (comparison runs)
-  static const bool force2 = std::getenv("HGF_STATS2") != nullptr && std::getenv("HGF_STATS2")[0] == '1';
+  const bool force2 = std::getenv("HGF_STATS2") != nullptr && std::getenv("HGF_STATS2")[0] == '1';
   if (!force2 && n <= kStats4MaxN && 64 + 2 * r <= 128 && stats4_smem(n, r) <= 200 * 1024) {
     switch (n) {
       case 1: return st4::stats4_impl<1>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
@@ -121,7 +121,7 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
   }
   // k_stats3 (Gram planes + warp-per-pixel recursion) where k_stats2 would spill heavily (n >= kStats3MinN)
   // or not fit its channel tiles in shared memory (the O(r) v1 kernel) -- measured on the C5 sweep
-  static const int s3min = std::getenv("HGF_STATS3_MIN_N") ? std::atoi(std::getenv("HGF_STATS3_MIN_N")) : kStats3MinN;
+  const int s3min = std::getenv("HGF_STATS3_MIN_N") ? std::atoi(std::getenv("HGF_STATS3_MIN_N")) : kStats3MinN;
   if (scratch3 && !aos && y0 == 0 && y1 == H && (n >= s3min || (n >= 7 && smem2 > 200 * 1024))) {
 #define CALL(N) st3::stats3_impl<N>(G, stats, scratch3, W, H, r, lam, mode, st)
     HGF_DISPATCH(n, CALL)

@@ -549,3 +549,24 @@ def test_shard_merge_against_oracle():
     check_labels(lab.cpu().numpy(), Z, s_v)
     check_z(cost.cpu().numpy(), Z.min(axis=0), s_v)
     assert torch.equal(peer_keys, keys)
+
+
+def test_two_stream_chunk_pipeline_bit_identical(monkeypatch):
+    """HGF_PIPELINE=1 (coefficients of chunk c + 1 on the handle stream while chunk c is aggregated on an aux stream,
+    the coefficient buffer split in two halves): bit-identical to the sequential chunk loop, incl. the fused merge."""
+    torch = _torch()
+    W, H, L = 208, 72, 150
+    scene = synth.make_stereo_scene(W, H, L, seed=78)
+    g = torch.from_numpy(scene.left).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    monkeypatch.setenv("HGF_COEF_BUDGET_MB", str(64 * 7 * 4 * H * W // (1 << 20) + 1))   # 64 labels per chunk
+    outs = []
+    for pipe in ("0", "1"):
+        monkeypatch.setenv("HGF_PIPELINE", pipe)
+        h = _hgf(W, H, 3, 2, 9, 0.05)
+        o = h.aggregate_wta_ex(g, vol, labels=True, min_cost=True, filtered=True, keys=True)
+        torch.cuda.synchronize()
+        outs.append(o)
+        h.close()
+    for k in ("labels", "min_cost", "filtered", "keys"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
