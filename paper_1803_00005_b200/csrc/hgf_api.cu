@@ -57,6 +57,12 @@ struct hgf_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_coef[2] = {nullptr, nullptr}, ev_agg[2] = {nullptr, nullptr}, ev_join = nullptr;
   hgf::WLayout wlay{};         // coefficient-buffer layout (rows pitched to 16 bytes when v3agg)
+  // few-label calls (L <= kSmallL, e.g. hgf_filter): the tile kernel k_coef2 on planar statistics and the planar
+  // k_agg3 instead of the lane-per-label k_coef5, which would keep 31 of its 32 lanes idle
+  bool small_ok = false;       // the planar maps below exist
+  bool planar_now = false;     // set by an entry point for the duration of a few-label call
+  hgf::WLayout wlay_planar{};
+  CUtensorMap tm_wp[2];
   bool v3coef = false;         // label-batched marching coefficient kernel (needs v3agg's layout, n <= 6)
   bool v4coef = false;         // tensor-core coefficient kernel (planar layout for k_agg3, n <= 6, r <= 9)
   bool v5coef = false;         // horizontal-first coefficient kernel (interleaved layout, n <= 6, r <= 9): default
@@ -79,6 +85,19 @@ namespace {
 
 // Every entry point that takes a handle runs on the handle's device (hgf.h: "bound to the CUDA device current
 // at create time"): switch to it for the call and restore the caller's current device on return.
+// Few-label mode for one call (see hgf_ctx::planar_now): on while the guard lives.
+constexpr int kSmallL = 2;
+struct SmallLMode {
+  hgf_ctx* h;
+  SmallLMode(hgf_ctx* hh, int L) : h(hh) {
+    const char* e = std::getenv("HGF_SMALL_L");
+    if (h) h->planar_now = h->small_ok && L <= kSmallL && !(e && e[0] == '0');
+  }
+  ~SmallLMode() {
+    if (h) h->planar_now = false;
+  }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(const hgf_ctx* h) {
@@ -202,8 +221,8 @@ hgf_status frame_stats(hgf_ctx* h, const float* guide, int y0, int y1) {
   e = traced(h, HGF_KC_STATS, h->stream, [&] {
     const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
     return hgf::launch_stats(h->n, h->G, h->stats, h->W, h->H, h->r, h->eps, h->mode,
-                             (h->v3coef || h->v4coef || h->v5coef) ? 1 : 0, lam0, y0, y1, h->st3_scratch,
-                             h->stream);
+                             ((h->v3coef || h->v4coef || h->v5coef) && !h->planar_now) ? 1 : 0, lam0, y0, y1,
+                             h->st3_scratch, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "stats");
   return HGF_OK;
@@ -256,6 +275,9 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
   const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
   if (!wdst) wdst = h->wbuf;
   return traced(h, HGF_KC_COEF, h->stream, [&] {
+    if (h->planar_now)
+      return hgf::launch_coef_fast(h->m, h->d, guide, h->stats, vol_chunk, h->wbuf, h->wlay_planar, h->W, h->H, h->r,
+                                   Lc, lam0, h->stream);
     if (h->v4coef) {
       CUtensorMap tm_vol;
       if (!encode_map_3d(&tm_vol, vol_chunk, h->W, h->H, Lc, (long long)h->W, (long long)h->W * h->H,
@@ -305,7 +327,9 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
 
 cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a, const void* tmaps = nullptr,
                              cudaStream_t st = nullptr) {
-  if (!tmaps) tmaps = h->tm_w;
+  if (h->planar_now)
+    return traced(h, HGF_KC_AGG, h->stream, [&] { return hgf::launch_agg_v3(h->n, h->r, h->tm_wp, a, h->stream); });
+  if (!tmaps) tmaps = h->planar_now ? h->tm_wp : h->tm_w;
   if (!st) st = h->stream;
   if (st != h->stream) {
     return traced(h, HGF_KC_AGG, st, [&] { return hgf::launch_agg_v3(h->n, h->r, tmaps, a, st); });
@@ -322,10 +346,13 @@ cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a, const void* tmap
 
 // TMA descriptor over the coefficient buffer for the v3 aggregation kernel (driver entry point via the
 // runtime, so the library does not link libcuda directly).
-bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out);
+bool make_wbuf_maps_layout(hgf_ctx* h, float* base, long long labels, const hgf::WLayout& wl, CUtensorMap* out);
+bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out) {
+  return make_wbuf_maps_layout(h, base, labels, h->wlay, out);
+}
 bool make_wbuf_tensor_map(hgf_ctx* h) { return make_wbuf_maps(h, h->wbuf, h->lcap, h->tm_w); }
 
-bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out) {
+bool make_wbuf_maps_layout(hgf_ctx* h, float* base, long long labels, const hgf::WLayout& wl, CUtensorMap* out) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
@@ -342,18 +369,18 @@ bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out)
     return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
   };
   int bx = 0, by = 0;
-  hgf::agg3_box(h->r, h->wlay.il, &bx, &by);
+  hgf::agg3_box(h->r, wl.il, &bx, &by);
   const int K = h->n + 1, KA = hgf::agg3_ka(K);
   for (int grp = 0; grp < 2; ++grp) {
     const cuuint32_t planes = (cuuint32_t)(grp == 0 ? KA : K - KA);
     CUresult r;
-    if (h->wlay.il) {
+    if (wl.il) {
       // rank 5 over the label-interleaved layout: (G px, 32 labels, x groups, y, label-batch planes); one
       // box = one label's planes of a BX x BY tile, 4G-byte inner runs, 64-byte swizzle (k_agg3's swz)
       const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
-      const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)h->H,
+      const cuuint64_t dims[5] = {G, NL, (cuuint64_t)wl.xg, (cuuint64_t)h->H,
                                   (cuuint64_t)(labels / hgf::kWGroupLabels) * K};
-      const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * h->H};
+      const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * wl.xg, G * NL * 4 * wl.xg * h->H};
       const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)(bx / G), (cuuint32_t)by, planes};
       const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
       r = encode(&out[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, base, dims, strides, box, estr,
@@ -361,9 +388,9 @@ bool make_wbuf_maps(hgf_ctx* h, float* base, long long labels, CUtensorMap* out)
                  hgf::kWGroupPx == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, wmap_l2_promotion(),
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
-      const cuuint64_t dims[3] = {(cuuint64_t)(h->W + h->wlay.pad), (cuuint64_t)(h->H + h->wlay.pad),
+      const cuuint64_t dims[3] = {(cuuint64_t)(h->W + wl.pad), (cuuint64_t)(h->H + wl.pad),
                                   (cuuint64_t)labels * K};
-      const cuuint64_t strides[2] = {(cuuint64_t)h->wlay.pitch * 4, (cuuint64_t)h->wlay.plane * 4};
+      const cuuint64_t strides[2] = {(cuuint64_t)wl.pitch * 4, (cuuint64_t)wl.plane * 4};
       const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, planes};
       const cuuint32_t estr[3] = {1, 1, 1};
       r = encode(&out[grp], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
@@ -384,7 +411,7 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
   // opt-in (HGF_PIPELINE=1): measured slower at C4 (36.3 vs 35.2 ms: the overlapped kernels slow each other down
   // -- coef 14.8 -> 20.5 ms, agg 19.2 -> 27.3 ms of device time -- on top of 4 chunks' tails instead of 2)
   const bool pipe_env = std::getenv("HGF_PIPELINE") && std::getenv("HGF_PIPELINE")[0] == '1';
-  if (h->half > 0 && !h->v5agg && L > h->half && pipe_env) {
+  if (h->half > 0 && !h->v5agg && !h->planar_now && L > h->half && pipe_env) {
     // ---- two-stream chunk pipeline: chunk c's coefficients go to half c % 2 of the buffer on the handle's
     // stream while chunk c - 1 is aggregated on the aux stream (the coefficient kernel is DRAM-bound, the
     // aggregation shared-memory-bound: running them side by side overlaps the two limits)
@@ -444,7 +471,7 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
       return cuda_fail(h, e, "join");
     return HGF_OK;
   }
-  if (h->v5agg && do_wta) {
+  if (h->v5agg && !h->planar_now && do_wta) {
     // k_agg5 merges every CTA's band minima into the frame's key buffer: start from the MIN identity
     cudaError_t e = traced(h, HGF_KC_KEYS, h->stream,
                            [&] { return hgf::launch_fill_i64(h->fkeys, HW, 0x7fffffffffffffffLL, h->stream); });
@@ -463,9 +490,10 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
     e = launch_coef_chunk(h, guide, chunk, Lc);
     if (e != cudaSuccess) return cuda_fail(h, e, "coef");
     hgf::AggArgs a{};
+    const hgf::WLayout& wl = h->planar_now ? h->wlay_planar : h->wlay;
     a.G = h->G;
     a.wbuf = h->wbuf;
-    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = h->wlay.pad; a.il = h->wlay.il;
+    a.W = h->W; a.H = h->H; a.r = h->r; a.L = Lc; a.pad = wl.pad; a.il = wl.il;
     a.label_base = label_offset + c0;
     a.filtered_out = filtered_out ? filtered_out + (long long)c0 * HW : nullptr;
     a.do_wta = do_wta;
@@ -481,7 +509,7 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
     e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
   }
-  if (h->v5agg && do_wta && (labels_out || min_cost_out || keys_out || h->peer_keys)) {
+  if (h->v5agg && !h->planar_now && do_wta && (labels_out || min_cost_out || keys_out || h->peer_keys)) {
     cudaError_t e = traced(h, HGF_KC_KEYS, h->stream, [&] {
       return hgf::launch_keys_finalize(h->fkeys, h->W, h->H, labels_out, min_cost_out, keys_out, h->peer_keys,
                                        h->rows_per_owner, h->stream);
@@ -634,6 +662,11 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
     h->v5coef = false;
     h->wlay = flat;
   }
+  if (h->v3agg && h->wlay.il && h->fast) {
+    // the planar layout in the same buffer (pitch ceil4(W) <= 16 ceil(W/16): fits every interleaved slot)
+    h->wlay_planar = padded;
+    h->small_ok = make_wbuf_maps_layout(h, h->wbuf, h->lcap, h->wlay_planar, h->tm_wp);
+  }
   if (h->v3agg && h->wlay.il && h->lcap >= 2 * hgf::kWGroupLabels) {
     // the two halves of the coefficient buffer for the two-stream chunk pipeline (slices_impl)
     h->half = (h->lcap / 2) / hgf::kWGroupLabels * hgf::kWGroupLabels;
@@ -700,6 +733,7 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
   if (dst == src || dst == guide) return fail(h, HGF_ERR_INVALID_ARGUMENT, "dst aliases an input");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
+  SmallLMode sm(h, 1);
   if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   return slices(h, guide, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
 }
@@ -718,6 +752,7 @@ hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* c
     return fail(h, HGF_ERR_INVALID_ARGUMENT, "no output requested");
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
+  SmallLMode sm(h, L);
   if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
   return slices(h, guide, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
@@ -965,6 +1000,7 @@ hgf_status hgf_segment(hgf_handle h, const float* image, const uint8_t* fg_seeds
     return hgf::launch_seg_cost(image, h->sg_counts, seeds, h->m, h->W, h->H, h->sg_cost, h->stream);
   });
   if (e != cudaSuccess) return cuda_fail(h, e, "segmentation cost");
+  SmallLMode sm(h, 2);
   if ((s = frame_stats(h, image, 0, h->H)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out) ? 1 : 0;
   return slices(h, image, h->sg_cost, 2, 0, filtered_out, do_wta, labels_out, min_cost_out, nullptr);

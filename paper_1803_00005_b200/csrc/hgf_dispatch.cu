@@ -171,7 +171,12 @@ namespace hgf {
 // Must match v2::RMAX in hgf_slice_v2.cuh (register arrays of k_agg2 are sized by it).
 constexpr int kV2RMax = 9;
 
-bool fast_path_ok(int m, int d, int r) { return m >= 1 && m <= 3 && d >= 1 && d <= 3 && r >= 1 && r <= kV2RMax; }
+// raw-guide channels x degree with a k_coef2 instantiation (hgf_inst2.cu): m, d <= 3, plus m = 4..6 at d = 1 and
+// m = 4 at d = 2 (BASELINE config 5 sweeps m up to 20 at d = 1; beyond these the generic kernels run)
+bool fast_path_ok(int m, int d, int r) {
+  const bool md = (m >= 1 && m <= 3 && d >= 1 && d <= 3) || (d == 1 && m >= 4 && m <= 6) || (m == 4 && d == 2);
+  return md && r >= 1 && r <= kV2RMax;
+}
 
 cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stats, const float* vol, float* wbuf, WLayout wo,
                              int W, int H, int r, int L, float lam0, cudaStream_t st) {
@@ -180,6 +185,7 @@ cudaError_t launch_coef_fast(int m, int d, const float* guide, const float* stat
     case 11: C2(1, 1); case 12: C2(1, 2); case 13: C2(1, 3);
     case 21: C2(2, 1); case 22: C2(2, 2); case 23: C2(2, 3);
     case 31: C2(3, 1); case 32: C2(3, 2); case 33: C2(3, 3);
+    case 41: C2(4, 1); case 51: C2(5, 1); case 61: C2(6, 1); case 42: C2(4, 2);
     default: return cudaErrorInvalidValue;
   }
 #undef C2

@@ -63,6 +63,13 @@ CASES = [
     ("il-n9", 100, 37, 3, 3, 20, 9, 0.05, "hgf"),
     ("il-n8-gf", 132, 29, 4, 2, 17, 4, 0.05, "gf"),
     ("il-n7", 68, 40, 7, 1, 33, 7, 1e-3, "hgf"),
+    # raw-guide channels m = 4..6 (degree 1) and m = 4 (degree 2): k_coef3 for L > 2, the planar k_coef2 path for
+    # the few-label calls (L <= 2), where round 1 fell back to the generic kernels
+    ("m6-d1", 100, 37, 6, 1, 20, 9, 0.05, "hgf"),
+    ("m5-d1-L2", 90, 47, 5, 1, 2, 4, 0.05, "gf"),
+    ("m4-d2-L1", 77, 41, 4, 2, 1, 7, 0.05, "hgf"),
+    ("m4-d2", 68, 40, 4, 2, 33, 7, 0.05, "gf"),
+    ("m6-d1-L1-r9", 130, 35, 6, 1, 1, 9, 0.05, "hgf"),
 ]
 
 
@@ -570,3 +577,22 @@ def test_two_stream_chunk_pipeline_bit_identical(monkeypatch):
         h.close()
     for k in ("labels", "min_cost", "filtered", "keys"):
         assert torch.equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.parametrize("m,d,L,path", [(3, 2, 1, "small"), (3, 2, 2, "small"), (3, 2, 3, "main"), (6, 1, 1, "small")])
+def test_few_label_path_matches_main_path_and_oracle(monkeypatch, m, d, L, path):
+    """Few-label calls (L <= 2: hgf_filter, segmentation) run k_coef2 on planar statistics + the planar k_agg3; the
+    result agrees with the oracle and, within fp32 rounding, with the lane-per-label main path (HGF_SMALL_L=0)."""
+    W, H = 150, 61
+    scene = synth.make_stereo_scene(W, H, max(L, 2), seed=31 * m + L)
+    I = scene.left if m == 3 else synth.smooth_guides(W, H, m, seed=8)
+    V = synth.stereo_cost_volume_np(scene, max(L, 2))[:L]
+    a = _run(np.ascontiguousarray(I), np.ascontiguousarray(V), d, 9, 0.05)
+    monkeypatch.setenv("HGF_SMALL_L", "0")
+    b = _run(np.ascontiguousarray(I), np.ascontiguousarray(V), d, 9, 0.05)
+    Z = O.hgf_filter(I, V, 0.05, 9, d)
+    s_v = float(np.abs(V).max())
+    check_z(a["filtered"], Z, s_v)
+    check_z(b["filtered"], Z, s_v)
+    check_labels(a["labels"], Z, s_v)
+    assert np.abs(a["filtered"] - b["filtered"]).max() <= 1e-4 * max(s_v, 1e-30)
