@@ -37,31 +37,6 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 // generic-proxy shared-memory writes -> visible to the tensor core's (async proxy) operand reads
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Instruction descriptor: kind::f16 with bf16 A and B (K-major), D f32, shape M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// D[tmem] (+)= A[tmem] x B[smem desc], bf16 inputs (K = 16 per instruction)
-__device__ __forceinline__ void mma_bf16_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-// x ~= hi + lo with hi = bf16(x), lo = bf16(x - hi) (|x - hi - lo| <= 2^-18 |x|), packed as bf16x2 with hi in
-// the low half (the even K element) and lo in the high half (the odd K element).
-__device__ __forceinline__ uint32_t split_bf16x2(float x) {
-  uint16_t h;
-  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
-  const float hf = __uint_as_float((uint32_t)h << 16);
-  uint32_t p;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(x - hf), "f"(x));
-  return p;
-}
-
 // D[tmem] (+)= A[tmem] x B[smem desc]
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
