@@ -35,7 +35,14 @@
 namespace hgf {
 namespace v3 {
 
-constexpr int TX = 64, TY = 24, KX = 8, NSEG = TX / KX, THREADS = 256, NOWN = TY * NSEG;
+constexpr int TX = 64, KX = 8, NSEG = TX / KX;
+// Tile height: 48 rows at one 512-thread CTA per SM for n <= HGF_AGG3_TALL_N (the 2R-row vertical halo then costs
+// 1.375x instead of 1.75x of TMA and vertical-pass traffic), else 24 rows at two 256-thread CTAs per SM.
+#ifndef HGF_AGG3_TALL_N
+#define HGF_AGG3_TALL_N 6
+#endif
+__host__ __device__ constexpr int agg3_ty(int NC) { return NC <= HGF_AGG3_TALL_N ? 48 : 24; }
+__host__ __device__ constexpr int agg3_threads(int NC) { return NC <= HGF_AGG3_TALL_N ? 512 : 256; }
 
 __host__ __device__ constexpr int box_pitch(int wx) {
   int b = (wx + 3) / 4 * 4;
@@ -50,6 +57,7 @@ struct AggGeom {
   static constexpr int WX = TX + 2 * R;
   static constexpr int VX = (WX + 31) / 32 * 32;                     // vertical-pass columns per plane
   static constexpr int BX = IL ? VX : box_pitch(WX);                   // IL: whole 128-B rows
+  static constexpr int TY = agg3_ty(NC), THREADS = agg3_threads(NC), NOWN = TY * NSEG;
   static constexpr int BY = TY + 2 * R;
   static constexpr int PLANE = BY * BX;                                // floats per plane in SMEM
   static constexpr int OFF_B = (KA * PLANE + 255) / 256 * 256;         // group B buffer: 1 KB aligned
@@ -92,7 +100,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 
 // tmA / tmB: tensor maps whose box covers planes [0, KA) / [KA, K) of one slice.
 template <int NC, int R, bool IL>
-__global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 ? 2 : 1)   // 2 CTAs/SM when the tile fits twice
+__global__ void __launch_bounds__(agg3_threads(NC), agg3_threads(NC) == 512 ? 1 : ((NC + 1) * 42 * 96 * 4 <= 113 * 1024 ? 2 : 1))
     k_agg3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ G, int W, int H, int pad, int L, int label_base, float* __restrict__ filtered_out,
            int do_wta, int first, int last, float* __restrict__ best_cost, int32_t* __restrict__ best_label,
@@ -100,6 +108,7 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
            long long* const* __restrict__ peer_keys, int rows_per_owner) {
   using Gm = AggGeom<NC, R, IL>;
   constexpr int K = Gm::K, KA = Gm::KA, BX = Gm::BX, BY = Gm::BY, PLANE = Gm::PLANE, NV4 = Gm::NV4;
+  constexpr int TY = Gm::TY, THREADS = Gm::THREADS, NOWN = Gm::NOWN;
   constexpr unsigned BYTES_A = Gm::KA * PLANE * 4u, BYTES_B = Gm::KB * PLANE * 4u;
   // Dynamic SMEM: group A buffer, group B buffer (1 KB aligned), then the two mbarriers.
   // Indexing the __shared__ array directly keeps every access in the shared state space (LDS/STS).
@@ -158,9 +167,10 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
   // planar: a quarter-warp = 8 rows of one segment (odd BX/4 pitch); IL: 4 rows x segments s, s + 2;
   // IL with the 32-byte swizzle: one row x all 8 segments (segments s and s + 4 share a chunk index and are
   // told apart by the swizzle bit; tools/swizzle_banks.py checks R = 1..32)
-  const int oy = IL ? (kSw32 ? (ln >> 3) + 4 * wq : (ln & 3) + 4 * wq) : (ln & 7) + 8 * (wq % 3);
+  constexpr int NRG = TY / 8;     // planar: row groups of 8 per segment half
+  const int oy = IL ? (kSw32 ? (ln >> 3) + 4 * wq : (ln & 3) + 4 * wq) : (ln & 7) + 8 * (wq % NRG);
   const int seg = IL ? (kSw32 ? (ln & 7) : ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1))
-                     : (ln >> 3) + 4 * (wq / 3);
+                     : (ln >> 3) + 4 * (wq / NRG);
   const int gy = y0 + oy;
   float g[NC > 0 ? NC : 1][KX];
   float invN[KX], best[KX];
@@ -187,83 +197,106 @@ __global__ void __launch_bounds__(THREADS, (NC + 1) * 42 * 96 * 4 <= 113 * 1024 
 #pragma unroll
   for (int q = 0; q < NV4; ++q) ofs[q] = swz<IL>(oy * BX + seg * KX + 4 * q);
   float z[KX];
-#pragma unroll 1
-  for (int l = 0; l < L; ++l) {
+  // per (label l, plane group h): the in-place vertical pass (all threads), then the owners' horizontal pass
+  auto vpass = [&](int h, int l) {
+    const int k0 = h == 0 ? 0 : KA, k1 = h == 0 ? KA : K;
+    float* lb = bufs[h];
+    mbar_wait(&bar[h], l & 1);
+    // ---- vertical window sums, in place: rows [0, TY) <- sum of rows [y, y + 2R]
+    for (int item = tid; item < (k1 - k0) * Gm::VX; item += THREADS) {
+      const int kk = item / Gm::VX, c = item % Gm::VX;
+      if (c >= Gm::WX) continue;
+      const int f0 = kk * PLANE + c;
+      // swizzled address of row y: (f0 ^ m(y)) + y*BX, the XOR mask m depending only on y mod 4
+      // (BX is a multiple of 32 floats, so adding y*BX never carries into the swizzled bits)
+      int fb[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k0 = h == 0 ? 0 : KA, k1 = h == 0 ? KA : K;
-      float* lb = bufs[h];
-      mbar_wait(&bar[h], l & 1);
-      // ---- vertical window sums, in place: rows [0, TY) <- sum of rows [y, y + 2R]
-      for (int item = tid; item < (k1 - k0) * Gm::VX; item += THREADS) {
-        const int kk = item / Gm::VX, c = item % Gm::VX;
-        if (c >= Gm::WX) continue;
-        const int f0 = kk * PLANE + c;
-        // swizzled address of row y: (f0 ^ m(y)) + y*BX, the XOR mask m depending only on y mod 4
-        // (BX is a multiple of 32 floats, so adding y*BX never carries into the swizzled bits)
-        int fb[4];
+      for (int j = 0; j < 4; ++j)
+        fb[j] = IL ? (kSw32 ? (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 1) << 2))
+                            : (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 3) << 2)))
+                   : f0;
+      // the column is read once; the outputs in two halves for 48-row tiles, the second half's input rows
+      // loaded after the first half's stores (rows below them), so at most ~TY/2 + 2R + 1 values are live
+      constexpr int VCH = TY > 24 ? TY / 2 : TY;
+      float col[BY];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          fb[j] = IL ? (kSw32 ? (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 1) << 2))
-                              : (f0 ^ ((((f0 >> 5) + j * (BX / 32)) & 3) << 2)))
-                     : f0;
-        float col[BY];
+      for (int y = 0; y < VCH + 2 * R; ++y) col[y] = lb[fb[y & 3] + y * BX];
+      float acc = 0.0f;
 #pragma unroll
-        for (int y = 0; y < BY; ++y) col[y] = lb[fb[y & 3] + y * BX];
-        float acc = 0.0f;
+      for (int y = 0; y <= 2 * R; ++y) acc += col[y];
+      lb[fb[0]] = acc;
 #pragma unroll
-        for (int y = 0; y <= 2 * R; ++y) acc += col[y];
-        lb[fb[0]] = acc;
+      for (int y = 1; y < VCH; ++y) {
+        acc += col[y + 2 * R] - col[y - 1];
+        lb[fb[y & 3] + y * BX] = acc;
+      }
+      if constexpr (VCH < TY) {
 #pragma unroll
-        for (int y = 1; y < TY; ++y) {
+        for (int y = VCH + 2 * R; y < BY; ++y) col[y] = lb[fb[y & 3] + y * BX];
+#pragma unroll
+        for (int y = VCH; y < TY; ++y) {
           acc += col[y + 2 * R] - col[y - 1];
           lb[fb[y & 3] + y * BX] = acc;
         }
       }
-      __syncthreads();
-      // ---- horizontal window sums, accumulated into Z (owners)
-      if (is_owner) {
+    }
+  };
+  auto hpass = [&](int h, int l) {
+    const int k0 = h == 0 ? 0 : KA;
+    float* lb = bufs[h];
+    // ---- horizontal window sums, accumulated into Z (owners)
+    if (is_owner) {
 #pragma unroll
-        for (int k = (h == 0 ? 0 : KA); k < (h == 0 ? KA : K); ++k) {
-          // plane kk of the group: swizzle mask of plane 0 flipped in bit 3 when kk * PLANE/32 = 2 mod 4
-          const int kk = k - k0;
-          // (32-byte swizzle: flipped in bit 2 when kk * PLANE/32 is odd)
-          const int flip = !IL ? 0
-                           : kSw32 ? (((kk * (PLANE / 32)) & 1) ? 4 : 0)
-                                   : ((((kk * ((PLANE / 32) & 3)) & 3) == 2) ? 8 : 0);
-          float f[4 * NV4];
+      for (int k = (h == 0 ? 0 : KA); k < (h == 0 ? KA : K); ++k) {
+        // plane kk of the group: swizzle mask of plane 0 flipped in bit 3 when kk * PLANE/32 = 2 mod 4
+        const int kk = k - k0;
+        // (32-byte swizzle: flipped in bit 2 when kk * PLANE/32 is odd)
+        const int flip = !IL ? 0
+                         : kSw32 ? (((kk * (PLANE / 32)) & 1) ? 4 : 0)
+                                 : ((((kk * ((PLANE / 32) & 3)) & 3) == 2) ? 8 : 0);
+        float f[4 * NV4];
 #pragma unroll
-          for (int q = 0; q < NV4; ++q) {
-            const float4 v = *reinterpret_cast<const float4*>(lb + kk * PLANE + (ofs[q] ^ flip));
-            f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
-          }
-          float acc = 0.0f;
-#pragma unroll
-          for (int dx = 0; dx <= 2 * R; ++dx) acc += f[dx];
-#pragma unroll
-          for (int s = 0; s < KX; ++s) {
-            if (s > 0) acc += f[s + 2 * R] - f[s - 1];
-            if (k == 0) z[s] = acc;
-            else z[s] = fmaf(g[k - 1][s], acc, z[s]);
-          }
+        for (int q = 0; q < NV4; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(lb + kk * PLANE + (ofs[q] ^ flip));
+          f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
         }
-        if (h == 1) {
+        float acc = 0.0f;
 #pragma unroll
-          for (int s = 0; s < KX; ++s) {
-            const int gx = x0 + seg * KX + s;
-            if (gy < H && gx >= 0 && gx < W) {
-              const float zz = z[s] * invN[s];
-              if (filtered_out) filtered_out[(long long)l * HW + (long long)gy * W + gx] = zz;
-              if (zz < best[s]) {
-                best[s] = zz;
-                bl[s] = label_base + l;
-              }
+        for (int dx = 0; dx <= 2 * R; ++dx) acc += f[dx];
+#pragma unroll
+        for (int s = 0; s < KX; ++s) {
+          if (s > 0) acc += f[s + 2 * R] - f[s - 1];
+          if (k == 0) z[s] = acc;
+          else z[s] = fmaf(g[k - 1][s], acc, z[s]);
+        }
+      }
+      if (h == 1) {
+#pragma unroll
+        for (int s = 0; s < KX; ++s) {
+          const int gx = x0 + seg * KX + s;
+          if (gy < H && gx >= 0 && gx < W) {
+            const float zz = z[s] * invN[s];
+            if (filtered_out) filtered_out[(long long)l * HW + (long long)gy * W + gx] = zz;
+            if (zz < best[s]) {
+              best[s] = zz;
+              bl[s] = label_base + l;
             }
           }
         }
       }
+    }
+  };
+#pragma unroll 1
+  for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      vpass(h, l);
       __syncthreads();
-      // group h of this slice consumed: fetch group h of the next slice while the other group is filtered
+      hpass(h, l);
+      __syncthreads();
+      // group h of this slice consumed: fetch group h of the next slice while the other group is filtered (a
+      // single-barrier variant that overlapped the next group's vertical pass with this group's owner work left
+      // the tile loads less time to land: 18.7 -> 20.5 ms at C4)
       if (tid == 0 && l + 1 < L) {
         fence_proxy_async();
         load(h, l + 1);
@@ -307,9 +340,10 @@ cudaError_t agg3_launch(const void* tmaps, const AggArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k_agg3<NC, R, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int XALIGN = IL ? kWGroupPx : 4;
-  dim3 grid((a.W + (XALIGN - R % XALIGN) % XALIGN + TX - 1) / TX, (a.H + TY - 1) / TY);
+  using Gm = AggGeom<NC, R, IL>;
+  dim3 grid((a.W + (XALIGN - R % XALIGN) % XALIGN + TX - 1) / TX, (a.H + Gm::TY - 1) / Gm::TY);
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmaps);
-  k_agg3<NC, R, IL><<<grid, THREADS, smem, st>>>(tm[0], tm[1], a.G, a.W, a.H, a.pad, a.L, a.label_base,
+  k_agg3<NC, R, IL><<<grid, Gm::THREADS, smem, st>>>(tm[0], tm[1], a.G, a.W, a.H, a.pad, a.L, a.label_base,
                                                  a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
                                                  a.best_label, a.labels_out, a.min_cost_out, a.keys_out,
                                                  a.peer_keys, a.rows_per_owner);

@@ -369,7 +369,7 @@ bool make_wbuf_maps_layout(hgf_ctx* h, float* base, long long labels, const hgf:
     return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
   };
   int bx = 0, by = 0;
-  hgf::agg3_box(h->r, wl.il, &bx, &by);
+  hgf::agg3_box(h->n, h->r, wl.il, &bx, &by);
   const int K = h->n + 1, KA = hgf::agg3_ka(K);
   for (int grp = 0; grp < 2; ++grp) {
     const cuuint32_t planes = (cuuint32_t)(grp == 0 ? KA : K - KA);

@@ -55,9 +55,9 @@ template cudaError_t agg3_impl<HGF_N, 8>(const void*, const AggArgs&, cudaStream
 template cudaError_t agg3_impl<HGF_N, 9>(const void*, const AggArgs&, cudaStream_t);
 }  // namespace v3
 #if HGF_N == 1
-void agg3_box(int R, int il, int* bx, int* by) {
+void agg3_box(int n, int R, int il, int* bx, int* by) {
   *bx = il ? (v3::TX + 2 * R + 31) / 32 * 32 : v3::box_pitch(v3::TX + 2 * R);
-  *by = v3::TY + 2 * R;
+  *by = v3::agg3_ty(n) + 2 * R;
 }
 #endif
 }  // namespace hgf

@@ -106,7 +106,7 @@ cudaError_t agg3_impl(const void* tmap, const AggArgs& a, cudaStream_t st);
 // k_agg3 fetches each slice's K planes as two TMA groups: [0, agg3_ka(K)) and [agg3_ka(K), K).
 __host__ __device__ constexpr int agg3_ka(int K) { return (K + 1) / 2; }
 // il = 1: label-interleaved layout (BX a multiple of 32 pixels; tensor-map box {16, 1, BX/16, BY, n+1}).
-void agg3_box(int R, int il, int* bx, int* by);
+void agg3_box(int n, int R, int il, int* bx, int* by);
 cudaError_t launch_agg_v3(int n, int r, const void* tmap, const AggArgs& a, cudaStream_t st);
 namespace v3 {
 template <int NC>
