@@ -493,23 +493,25 @@ def main():
                 "peak_basis": ("148 SMs x 128 FP32 lanes x 2 (FMA) x 1965 MHz (B200_PROFILING.md unit counts/clock)"
                                if dom != "stats" else "148 SMs x 64 FP64 lanes x 2 x 1965 MHz"),
                 "share_of_step": dom_ms / (ms_max if world == 1 else ms) if ms else None}
-    # the pipe that binds the slice kernels in this design: the SM's L1/shared-memory data pipe, one 128-byte
-    # wavefront per clock per SM (B200_PROFILING.md); ncu's per-launch shared-memory wavefront counts of each
-    # slice kernel (profiles/ncu_smem.json) over its live average launch time
+    # the pipe that binds the aggregation kernel in this design: the SM's L1/shared-memory data pipe, one 128-byte
+    # wavefront per clock per SM (B200_PROFILING.md); ncu's per-launch shared-memory wavefront counts of each slice
+    # kernel (profiles/ncu_traffic.json, used only for the kernels this handle runs) over its live launch time
     smem_pipe = None
-    spath = os.path.join(ROOT, "profiles", "ncu_smem.json")
-    if os.path.exists(spath):
+    if os.path.exists(tpath):
         try:
-            sj = json.load(open(spath)).get(c["name"], {})
+            tj = json.load(open(tpath))
+            sj = tj.get(c["name"], {})
             wpeak = SM_COUNT * 1965e6 / 1e9
-            smem_pipe = {"unit": "G wavefronts/s (128 B each)", "peak": wpeak,
+            smem_pipe = {"unit": "G wavefronts/s (128 B each)", "peak": wpeak, "source": tj.get("_commit"),
                          "basis": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per launch / live launch time; "
                                   "peak 1 wavefront/clk/SM x 148 SMs x 1965 MHz; TMA writes not counted"}
+            path_kernels = {"coef": h.kernel_path.split("+")[0], "agg": h.kernel_path.split("+")[1]}
             for k in ("coef", "agg"):
                 kms, kcnt = prof[k]
-                if k in sj and kcnt:
-                    ach = sj[k] / (kms / kcnt / 1e3) / 1e9
-                    smem_pipe[k] = {"achieved": ach, "frac": ach / wpeak}
+                ent = sj.get(k)
+                if isinstance(ent, dict) and ent.get("kernel", "").startswith("k_" + path_kernels[k]) and kcnt:
+                    ach = ent["smem_wavefronts_per_launch"] / (kms / kcnt / 1e3) / 1e9
+                    smem_pipe[k] = {"kernel": ent["kernel"], "achieved": ach, "frac": ach / wpeak}
         except Exception:
             smem_pipe = None
     stage_ms = {k: v[0] / args.steps for k, v in prof.items()}
