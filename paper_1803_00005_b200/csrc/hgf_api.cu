@@ -68,6 +68,8 @@ struct hgf_ctx {
   bool v5coef = false;         // horizontal-first coefficient kernel (interleaved layout, n <= 6, r <= 9): default
   CUtensorMap tm_g5;           // TMA descriptor over the raw guide planes of G for k_coef5 (box 164 x 1 x m)
   bool v5agg = false;          // row-marching aggregation k_agg5 (default after k_coef5, n <= 6, r <= 9)
+  bool v6agg = false;          // warp-specialised aggregation k_agg6 (default on the interleaved layout, n <= 6)
+  CUtensorMap tm_w6;           // k_agg6: rank-5 map over wbuf, one-plane box, 64-byte swizzle
   CUtensorMap tm_w5;           // k_agg5: rank-5 map over wbuf, box (16, 4, 6, 1, n + 1), 64-byte swizzle
   CUtensorMap tm_ga5;          // k_agg5: map over G (W, H, n), box (64, 1, n)
   int64_t* fkeys = nullptr;    // k_agg5: the frame's per-pixel minimum keys [H][W] (signed order, hgf.h)
@@ -339,6 +341,7 @@ cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a, const void* tmap
       return hgf::launch_agg_v5(h->n, &h->tm_w5, &h->tm_ga5, h->W, h->H, h->r, a.L, a.label_base,
                                 hgf::kWGroupLabels, reinterpret_cast<unsigned long long*>(h->fkeys), a.filtered_out,
                                 h->stream);
+    if (h->v6agg) return hgf::launch_agg_v6(h->n, h->r, &h->tm_w6, a, h->stream);
     if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, h->tm_w, a, h->stream);
     return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
   });
@@ -548,9 +551,9 @@ const char* hgf_kernel_path(hgf_handle h) {
   if (!h) return "";
   if (h->v3agg) {
     if (h->v5agg) return "coef5+agg5";
-    if (h->v5coef) return "coef5+agg3";
+    if (h->v5coef) return h->v6agg ? "coef5+agg6" : "coef5+agg3";
     if (h->v4coef) return "coef4+agg3";
-    if (h->v3coef) return "coef3+agg3";
+    if (h->v3coef) return h->v6agg ? "coef3+agg6" : "coef3+agg3";
     return "coef2+agg3";
   }
   return h->fast ? "coef2+agg2" : "coef1+agg1";
@@ -699,6 +702,22 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
         h->v5agg = false;
       }
     }
+  }
+  if (h->v3agg && h->wlay.il && !h->v5agg && h->n <= hgf::kAgg6MaxN && h->r <= 9 && hgf::kWGroupPx == 16) {
+    // k_agg6 (default; HGF_AGG6=0 keeps k_agg3): the same tile with one TMA box per coefficient plane
+    const char* f = std::getenv("HGF_AGG6");
+    auto encode = tensor_map_encoder();
+    const cuuint64_t G = hgf::kWGroupPx, NL = hgf::kWGroupLabels;
+    const cuuint64_t dims[5] = {G, NL, (cuuint64_t)h->wlay.xg, (cuuint64_t)H,
+                                (cuuint64_t)(h->lcap / hgf::kWGroupLabels) * K};
+    const cuuint64_t strides[4] = {G * 4, G * NL * 4, G * NL * 4 * h->wlay.xg, G * NL * 4 * h->wlay.xg * H};
+    const cuuint32_t box[5] = {(cuuint32_t)G, 1, (cuuint32_t)((64 + 2 * h->r + 31) / 32 * 32 / G),
+                               (cuuint32_t)(hgf::kAgg6TY + 2 * h->r), 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    h->v6agg = !(f && f[0] == '0') && encode &&
+               encode(&h->tm_w6, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, h->wbuf, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   *out = h;
   return HGF_OK;

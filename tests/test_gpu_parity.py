@@ -97,10 +97,10 @@ def test_aggregate_parity(name, W, H, m, d, L, r, lam, mode):
 
 def test_c2_full_parity():
     """BASELINE config 2 in full: 450x375 Middlebury size, degree-2 RGB (n = 6), 60 labels, r = 9 -- on the
-    default k_coef5 -> k_agg3 path (W % 4 != 0: each chunk is repacked into 452-float rows for the TMA)."""
+    default k_coef5 -> k_agg6 path (W % 4 != 0: each chunk is repacked into 452-float rows for the TMA)."""
     c = synth.config("C2")
     h = _hgf(c["W"], c["H"], c["m"], c["d"], c["r"], c["lam"])
-    assert h.kernel_path == "coef5+agg3", h.kernel_path
+    assert h.kernel_path == "coef5+agg6", h.kernel_path
     h.close()
     scene = synth.make_stereo_scene(c["W"], c["H"], c["L"], c["seed"])
     V = synth.stereo_cost_volume_np(scene, c["L"])
@@ -459,6 +459,7 @@ def test_tma_l2_promotion_knob_is_bit_identical(promo, monkeypatch):
     scene = synth.make_stereo_scene(W, H, L, seed=77)
     g = torch.from_numpy(scene.left).cuda()
     vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    monkeypatch.setenv("HGF_AGG6", "0")        # the knob applies to k_agg3's maps
     monkeypatch.delenv("HGF_TMA_L2PROMO", raising=False)
     h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
     a = h.aggregate_wta_ex(g, vol, labels=True, filtered=True)
@@ -478,14 +479,16 @@ def test_tma_l2_promotion_knob_is_bit_identical(promo, monkeypatch):
 # steps without a restart), with the stereo-like and the iid near-tie distributions; k_coef3 at the same band length.
 BAND_CASES = [
     # (name, W, H, L, distribution, env, expected kernel path)
-    ("coef5-3strips-3bands-2batches", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
-    ("coef5-iid-band270", 260, 560, 34, "iid", {"HGF_COEF5_BH": "270"}, "coef5+agg3"),
+    ("coef5-3strips-3bands-2batches", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270"}, "coef5+agg6"),
+    ("coef5-iid-band270", 260, 560, 34, "iid", {"HGF_COEF5_BH": "270"}, "coef5+agg6"),
+    # k_agg3 (HGF_AGG6=0) on the same interleaved layout
+    ("coef5-agg3-band270", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270", "HGF_AGG6": "0"}, "coef5+agg3"),
     # the opt-in row-marching aggregation (k_agg5) at its band length: 3 bands x 2 label groups
     ("coef5-agg5", 300, 560, 40, "stereo", {"HGF_COEF5_BH": "270", "HGF_AGG5": "1", "HGF_AGG5_BH": "270"},
      "coef5+agg5"),
-    ("coef3-band270", 300, 560, 40, "stereo", {"HGF_COEF5": "0", "HGF_COEF3_BH": "270"}, "coef3+agg3"),
+    ("coef3-band270", 300, 560, 40, "stereo", {"HGF_COEF5": "0", "HGF_COEF3_BH": "270"}, "coef3+agg6"),
     # W % 4 != 0 on k_coef5 (repacked rows; odd width: the guide pairs' own pitch), 3 strips
-    ("coef5-odd-width", 301, 140, 40, "stereo", {}, "coef5+agg3"),
+    ("coef5-odd-width", 301, 140, 40, "stereo", {}, "coef5+agg6"),
 ]
 
 
@@ -513,10 +516,10 @@ def test_full_frame_band_geometry(monkeypatch, name, W, H, L, dist, env, path):
 
 
 def test_default_kernel_path_is_coef5():
-    """The headline configs (RGB degree 2, r = 9, W % 4 == 0) run k_coef5 -> k_agg3 by default."""
+    """The headline configs (RGB degree 2, r = 9, W % 4 == 0 or not) run k_coef5 -> k_agg6 by default."""
     for W, H in ((3840, 2160), (1920, 1080), (452, 375), (450, 375), (451, 77)):
         h = _hgf(W, H, 3, 2, 9, 0.05)
-        assert h.kernel_path == "coef5+agg3", (W, H, h.kernel_path)
+        assert h.kernel_path == "coef5+agg6", (W, H, h.kernel_path)
         h.close()
 
 
@@ -597,3 +600,45 @@ def test_few_label_path_matches_main_path_and_oracle(monkeypatch, m, d, L, path)
     check_z(b["filtered"], Z, s_v)
     check_labels(a["labels"], Z, s_v)
     assert np.abs(a["filtered"] - b["filtered"]).max() <= 1e-4 * max(s_v, 1e-30)
+
+
+# k_agg6 (warp-specialised, per-plane pipeline) performs k_agg3's arithmetic in the same order: bit-identical
+# filtered costs, labels, minimum costs and keys, over ragged tiles, several 32-label groups, multi-chunk WTA
+# carries (small HGF_COEF_BUDGET_MB) and radii 1..9; k_agg6 also against the oracle on the smaller cases.
+AGG6_CASES = [
+    # (W, H, L, m, d, r, budget MB)
+    (208, 72, 40, 3, 2, 9, None),
+    (301, 101, 70, 3, 2, 9, "1"),
+    (77, 53, 5, 3, 2, 9, None),
+    (160, 97, 33, 1, 2, 4, None),
+    (96, 130, 12, 2, 3, 1, None),
+    (128, 64, 9, 6, 1, 7, None),
+]
+
+
+@pytest.mark.parametrize("W,H,L,m,d,r,budget", AGG6_CASES)
+def test_agg6_bit_identical_to_agg3(monkeypatch, W, H, L, m, d, r, budget):
+    torch = _torch()
+    scene = synth.make_stereo_scene(W, H, L, seed=W + L)
+    I = np.ascontiguousarray(synth.smooth_guides(W, H, m, seed=W)) if m != 3 else scene.left
+    g = torch.from_numpy(I).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    if budget:
+        monkeypatch.setenv("HGF_COEF_BUDGET_MB", budget)
+    out = {}
+    for agg6 in ("1", "0"):
+        monkeypatch.setenv("HGF_AGG6", agg6)
+        h = _hgf(W, H, m, d, r, 0.05)
+        assert h.kernel_path.endswith("+agg6" if agg6 == "1" else "+agg3"), h.kernel_path
+        o = h.aggregate_wta_ex(g, vol, labels=True, min_cost=True, keys=True, filtered=True)
+        torch.cuda.synchronize()
+        out[agg6] = {k: v.cpu().numpy() for k, v in o.items()}
+        h.close()
+    a, b = out["1"], out["0"]
+    for k in ("filtered", "labels", "min_cost", "keys"):
+        assert np.array_equal(a[k], b[k]), k
+    if W * H * L <= 208 * 72 * 40:
+        V = synth.stereo_cost_volume_np(scene, L)
+        Z = O.hgf_filter(I, V, 0.05, r, d)
+        check_z(a["filtered"], Z, float(np.abs(V).max()))
+        check_labels(a["labels"], Z, float(np.abs(V).max()))
