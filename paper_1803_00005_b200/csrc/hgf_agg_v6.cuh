@@ -18,7 +18,10 @@
 //   * warps 0..11 (owners: row x 8 pixels, k_agg3's conflict-free swizzled mapping) wait on vdone[k], do the
 //     horizontal sums, Z and (after the last plane) the WTA, then arrive on hdone[k].
 // The vertical warps run ahead of the owners by up to a slice, so both passes keep the LSU busy without CTA
-// barriers.  Each barrier completes once per slice, so its phase parity is l & 1.
+// barriers.  vdone / hdone complete once per slice (phase parity l & 1).  With two vertical teams (alternate
+// plane-steps s = lK + k) plane k's TMA for slice l signals full[k][l % 2], which only one team waits on, in slice
+// order (parity (l / 2) & 1): a parity wait must never run two phases ahead of the barrier, which a single
+// full[k] shared by both teams would allow.
 #pragma once
 #include <cuda.h>
 
@@ -30,11 +33,19 @@
 namespace hgf {
 namespace v6a {
 
-constexpr int TX = 64, TY = 48, KX = 8, NSEG = TX / KX;
-constexpr int NOWN = TY * NSEG;            // 384 owner threads = warps 0..11
-constexpr int NVW = 3;                     // vertical warps 12..14
-constexpr int THREADS = 512;               // + producer warp 15
-static_assert(NOWN + 32 * NVW + 32 == THREADS, "warp roles");
+// Tile height (HGF_AGG6_TY, = kAgg6TY): 48 rows -> 12 owner warps and one vertical team of 3 warps; 36 rows -> 9
+// owner warps and two vertical teams (alternate plane-steps), for 1.5x instead of 1.375x vertical halo: measured
+// the same C4 time (17.05 vs 17.0 ms per frame), so 48 (bit-identical to k_agg3's 48-row tiles).
+#ifndef HGF_AGG6_TY
+#define HGF_AGG6_TY 48
+#endif
+constexpr int TX = 64, TY = HGF_AGG6_TY, KX = 8, NSEG = TX / KX;
+constexpr int NOWN = TY * NSEG;            // owner threads = warps [0, NOWN / 32)
+constexpr int NVW = 3;                     // warps per vertical team (one column each of the 96-column tile)
+constexpr int THREADS = 512;               // the last warp is the TMA producer
+constexpr int NVT = (THREADS / 32 - 1 - NOWN / 32) / NVW;   // vertical teams
+static_assert(NOWN % 32 == 0 && NVT >= 1 && NOWN + 32 * NVW * NVT + 32 == THREADS, "warp roles");
+static_assert(TY == kAgg6TY, "host box height");
 static_assert(kWGroupPx == 16, "64-byte swizzle (16-pixel groups)");
 
 template <int NC, int R>
@@ -72,7 +83,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PSTRIDE = Gm::PSTRIDE, NV4 = Gm::NV4;
   extern __shared__ __align__(1024) float buf[];
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + Gm::FLOATS);
-  uint64_t* vdone = full + K;
+  uint64_t* vdone = full + K * NVT;   // full[k * NVT + l % NVT]: see below
   uint64_t* hdone = vdone + K;
   const int tid = threadIdx.x, wq = tid >> 5, ln = tid & 31;
   // tile origin shifted so the TMA x coordinate x0 - R is a whole 16-pixel group (unaligned x traps); grouped
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (tid == 0) {
     for (int k = 0; k < K; ++k) {
-      mbar_init(&full[k], 1);
+      for (int t = 0; t < NVT; ++t) mbar_init(&full[k * NVT + t], 1);
       mbar_init(&vdone[k], NVW);
       mbar_init(&hdone[k], NOWN / 32);
     }
@@ -104,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   const int S = K * L;
 
-  if (wq == 15) {
+  if (wq == THREADS / 32 - 1) {
     // ---- producer: plane k of slice l into buffer k once the owners have released slice l - 1's plane k
     if (ln != 0) return;
     for (int s = 0; s < S; ++s) {
@@ -114,27 +125,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         cuda::ptx::fence_proxy_async(cuda::ptx::space_shared);
       }
       cuda::ptx::mbarrier_arrive_expect_tx(cuda::ptx::sem_release, cuda::ptx::scope_cta, cuda::ptx::space_shared,
-                                           &full[k], (uint32_t)(Gm::PLANE * 4));
+                                           &full[k * NVT + l % NVT], (uint32_t)(Gm::PLANE * 4));
       const int32_t c[5] = {0, l % kWGroupLabels, tx0 / kWGroupPx, ty0, (l / kWGroupLabels) * K + k};
       cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, buf + k * PSTRIDE, &tm, c,
-                                      &full[k]);
+                                      &full[k * NVT + l % NVT]);
     }
     return;
   }
 
   if (wq >= NOWN / 32) {
+    const int team = (wq - NOWN / 32) / NVW;
     // ---- vertical warps: column c of every plane, in place: rows [0, TY) <- sum of rows [y, y + 2R].  The whole
     // column is loaded before the first sum (one shared-memory round trip per plane); same summation order as
     // k_agg3, so the two kernels are bit-identical.  (Two independent half-column chains were measured: no gain.)
-    const int c = tid - NOWN;
+    const int c = tid - NOWN - 32 * NVW * team;
     // swizzled address of row y: (c ^ m(y)) + y*BX, the XOR mask depending only on y mod 4 (BX = 96 floats)
     int fb[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) fb[j] = c ^ ((((c >> 5) + j * (BX / 32)) & 3) << 2);
-    for (int s = 0; s < S; ++s) {
+    for (int s = team; s < S; s += NVT) {
       const int l = s / K, k = s - l * K;
       float* lb = buf + k * PSTRIDE;
-      mbar_wait(&full[k], l & 1);
+      mbar_wait(&full[k * NVT + l % NVT], (l / NVT) & 1);
       if (c < Gm::WX) {
         float col[BY];
 #pragma unroll
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <int NC, int R>
 cudaError_t agg6_launch(const void* tmap, const AggArgs& a, cudaStream_t st) {
   using Gm = Geom<NC, R>;
-  const size_t smem = (size_t)Gm::FLOATS * 4 + 3 * Gm::K * sizeof(uint64_t);
+  const size_t smem = (size_t)Gm::FLOATS * 4 + (2 + NVT) * Gm::K * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(k_agg6<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int XSHIFT = (kWGroupPx - R % kWGroupPx) % kWGroupPx;

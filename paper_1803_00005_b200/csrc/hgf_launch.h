@@ -140,10 +140,13 @@ constexpr int kCoef5BoxX = 164, kCoef5LB = 32, kCoef5MaxN = 6;
 constexpr int kAgg5LB = 4, kAgg5MaxN = 6;
 cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int H, int r, int L, int label_base,
                           int labels_per_cta, unsigned long long* keys, float* filtered_out, cudaStream_t st);
-// Warp-specialised aggregation (hgf_agg_v6.cuh, instantiated in hgf_agg6.cu): k_agg3's 64 x 48 tile on the
+// Warp-specialised aggregation (hgf_agg_v6.cuh, instantiated in hgf_agg6.cu): 64 x kAgg6TY tiles on the
 // label-interleaved layout, n <= 6, r <= 9; tm: rank-5 map over the coefficient buffer with a one-plane box
-// (16, 1, ceil32(64 + 2r) / 16, 48 + 2r, 1), 64-byte swizzle.  Same AggArgs contract as k_agg3 (a.il == 1).
-constexpr int kAgg6MaxN = 6, kAgg6TY = 48;
+// (16, 1, ceil32(64 + 2r) / 16, kAgg6TY + 2r, 1), 64-byte swizzle.  Same AggArgs contract as k_agg3 (a.il == 1).
+#ifndef HGF_AGG6_TY
+#define HGF_AGG6_TY 48
+#endif
+constexpr int kAgg6MaxN = 6, kAgg6TY = HGF_AGG6_TY;
 cudaError_t launch_agg_v6(int n, int r, const void* tm, const AggArgs& a, cudaStream_t st);
 // keys[H][W] -> labels_out / min_cost_out / keys_out (each nullable) and, when peer_keys != null, a system-scope
 // 64-bit atomic MIN of every pixel's key into the row owner's buffer (the fused label-sharded merge).
