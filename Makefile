@@ -9,7 +9,7 @@ CS := $(PKG)/csrc
 NS := 1 2 3 4 5 6 7 8 9 10 11 12 13 14 15 16 17 18 19 20
 DEPS := $(wildcard $(CS)/*.cuh) $(wildcard $(CS)/*.h) include/hgf.h
 MDS := 1_1 1_2 1_3 2_1 2_2 2_3 3_1 3_2 3_3 4_1 5_1 6_1 4_2
-OBJ := build/hgf_api.o build/hgf_dispatch.o build/hgf_stereo.o build/hgf_coef5.o build/hgf_agg5.o build/hgf_agg6.o $(foreach n,$(NS),build/inst_$(n).o) $(foreach md,$(MDS),build/inst2_$(md).o)
+OBJ := build/hgf_api.o build/hgf_dispatch.o build/hgf_stereo.o build/hgf_coef5.o build/hgf_agg5.o build/hgf_agg6.o build/hgf_agg6w.o $(foreach n,$(NS),build/inst_$(n).o) $(foreach md,$(MDS),build/inst2_$(md).o)
 LIB := $(PKG)/libhgf.so
 
 all: $(LIB)

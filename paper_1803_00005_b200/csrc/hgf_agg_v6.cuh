@@ -39,18 +39,36 @@ namespace v6a {
 #ifndef HGF_AGG6_TY
 #define HGF_AGG6_TY 48
 #endif
-constexpr int TX = 64, TY = HGF_AGG6_TY, KX = 8, NSEG = TX / KX;
-constexpr int NOWN = TY * NSEG;            // owner threads = warps [0, NOWN / 32)
+constexpr int TX = 64, TY = HGF_AGG6_TY;
 constexpr int NVW = 3;                     // warps per vertical team (one column each of the 96-column tile)
-constexpr int THREADS = 512;               // the last warp is the TMA producer
-constexpr int NVT = (THREADS / 32 - 1 - NOWN / 32) / NVW;   // vertical teams
-static_assert(NOWN % 32 == 0 && NVT >= 1 && NOWN + 32 * NVW * NVT + 32 == THREADS, "warp roles");
 static_assert(TY == kAgg6TY, "host box height");
 static_assert(kWGroupPx == 16, "64-byte swizzle (16-pixel groups)");
 
-template <int NC, int R>
+// Owner configuration.  D = 0: owners of 8 pixels holding the n guidance planes G_k (any n <= 6), 512 threads.
+// D >= 1: owners of 16 pixels holding only the m = NC / D raw channels I_i (G_{(i-1)D+j} = I_i^j formed by the same
+// repeated multiplication as k_poly_guidance, so bit-identical), m <= 3: half the owners, each loading 16 + 2R
+// columns per plane for 16 outputs instead of 8 + 2R for 8 (-35 % of the horizontal pass's shared wavefronts), at
+// 320 threads so the wider owners get ~200 registers.  Either way the owner's horizontal sums restart every 8
+// pixels, as k_agg3's owners do.
+template <int NC, int D>
+struct Roles {
+  static constexpr int KX = D == 0 ? 8 : 16, NSEG = TX / KX;
+  static constexpr int NOWN = TY * NSEG;             // owner threads = warps [0, NOWN / 32)
+  static constexpr int THREADS = D == 0 ? 512 : NOWN + 32 * NVW + 32;   // the last warp is the TMA producer
+  static constexpr int NVT = (THREADS / 32 - 1 - NOWN / 32) / NVW;     // vertical teams
+  static constexpr int MG = D == 0 ? NC : NC / (D > 0 ? D : 1);    // guide values held per owner pixel
+  static_assert(NOWN % 32 == 0 && NVT >= 1 && NOWN + 32 * NVW * NVT + 32 == THREADS, "warp roles");
+  static_assert(D == 0 || (NC % (D > 0 ? D : 1) == 0 && NC / (D > 0 ? D : 1) <= 3), "raw-channel owners: m <= 3");
+  // registers per thread: each SM sub-partition holds 16384, and takes up to ceil(warps / 4) of the CTA's warps
+  static constexpr int MAXREG = (16384 / (32 * ((THREADS / 32 + 3) / 4))) / 8 * 8 > 255
+                                    ? 255
+                                    : (16384 / (32 * ((THREADS / 32 + 3) / 4))) / 8 * 8;
+};
+
+template <int NC, int R, int D>
 struct Geom {
   static constexpr int K = NC + 1;
+  static constexpr int KX = Roles<NC, D>::KX, NSEG = Roles<NC, D>::NSEG;
   static constexpr int WX = TX + 2 * R;
   static constexpr int BX = (WX + 31) / 32 * 32;
   static constexpr int BY = TY + 2 * R;
@@ -73,14 +91,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // tm: rank-5 map over the interleaved coefficient buffer, box (16 px, 1 label, BX/16 groups, BY rows, 1 plane).
-template <int NC, int R>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NC, int R, int D>
+__global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     k_agg6(const __grid_constant__ CUtensorMap tm, const float* __restrict__ G, int W, int H, int L, int label_base,
            float* __restrict__ filtered_out, int do_wta, int first, int last, float* __restrict__ best_cost,
            int32_t* __restrict__ best_label, int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out,
            int64_t* __restrict__ keys_out, long long* const* __restrict__ peer_keys, int rows_per_owner) {
-  using Gm = Geom<NC, R>;
-  constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PSTRIDE = Gm::PSTRIDE, NV4 = Gm::NV4;
+  using Gm = Geom<NC, R, D>;
+  using Ro = Roles<NC, D>;
+  constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PSTRIDE = Gm::PSTRIDE, NV4 = Gm::NV4, KX = Gm::KX;
+  constexpr int NOWN = Ro::NOWN, THREADS = Ro::THREADS, NVT = Ro::NVT, MG = Ro::MG;
   extern __shared__ __align__(1024) float buf[];
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + Gm::FLOATS);
   uint64_t* vdone = full + K * NVT;   // full[k * NVT + l % NVT]: see below
@@ -167,12 +187,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     return;
   }
 
-  // ---- owners: row oy, pixels x0 + 8*seg + [0, 8); a quarter-warp = 4 rows x segments s, s + 2 (conflict-free
-  // 128-bit loads under the 64-byte swizzle, tools/swizzle_banks.py)
-  const int oy = (ln & 3) + 4 * wq;
-  const int seg = ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1);
+  // ---- owners: row oy, pixels x0 + KX*seg + [0, KX).  D = 0: a quarter-warp = 4 rows x segments s, s + 2; D >= 1:
+  // 4 rows x 2 segments of one 8-row block.  Both conflict-free for the 128-bit loads under the 64-byte swizzle
+  // (tools/swizzle_banks.py).
+  const int oy = D == 0 ? (ln & 3) + 4 * wq : (ln & 3) + 4 * (ln >> 4) + 8 * wq;
+  const int seg = D == 0 ? ((ln >> 3) & 1) + 4 * (ln >> 4) + 2 * ((ln >> 2) & 1) : (ln >> 2) & 3;
   const int gy = y0 + oy;
-  float g[NC][KX];
+  float g[MG][KX];
   float invN[KX], best[KX];
   int32_t bl[KX];
 #pragma unroll
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool in = gy < H && gx >= 0 && gx < W;
     const long long p = in ? (long long)gy * W + gx : 0;
 #pragma unroll
-    for (int k = 0; k < NC; ++k) g[k][j] = in ? __ldg(G + k * HW + p) : 0.0f;
+    for (int k = 0; k < MG; ++k) g[k][j] = in ? __ldg(G + (long long)(D == 0 ? k : k * D) * HW + p) : 0.0f;
     invN[j] = in ? 1.0f / (float)window_count(gy, gx, H, W, R) : 0.0f;
     best[j] = INFINITY;
     bl[j] = 0;
@@ -190,6 +211,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       bl[j] = best_label[p];
     }
   }
+  // G_k at pixel s (k >= 1): the held plane, or I_i^j by repeated multiplication (k_poly_guidance's order)
+  auto guide = [&](int k, int s) -> float {
+    if constexpr (D == 0) {
+      return g[k - 1][s];
+    } else {
+      const int i = (k - 1) / D, j = (k - 1) % D;
+      float t = g[i][s];
+#pragma unroll
+      for (int e = 0; e < j; ++e) t = t * g[i][s];
+      return t;
+    }
+  };
   int ofs[NV4];
 #pragma unroll
   for (int q = 0; q < NV4; ++q) {
@@ -209,14 +242,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float4 v = *reinterpret_cast<const float4*>(lb + ofs[q]);
         f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
       }
-      float acc = 0.0f;
+      // horizontal window sums, restarted every 8 pixels (k_agg3's owner order)
 #pragma unroll
-      for (int dx = 0; dx <= 2 * R; ++dx) acc += f[dx];
+      for (int h8 = 0; h8 < KX; h8 += 8) {
+        float acc = 0.0f;
 #pragma unroll
-      for (int s = 0; s < KX; ++s) {
-        if (s > 0) acc += f[s + 2 * R] - f[s - 1];
-        if (k == 0) z[s] = acc;
-        else z[s] = fmaf(g[k - 1][s], acc, z[s]);
+        for (int dx = 0; dx <= 2 * R; ++dx) acc += f[h8 + dx];
+#pragma unroll
+        for (int s = h8; s < h8 + 8; ++s) {
+          if (s > h8) acc += f[s + 2 * R] - f[s - 1];
+          if (k == 0) z[s] = acc;
+          else z[s] = fmaf(guide(k, s), acc, z[s]);
+        }
       }
       // release the plane once its loaded values have been consumed
       __syncwarp();
@@ -259,20 +296,33 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (last && peer_keys) __threadfence_system();
 }
 
-template <int NC, int R>
+template <int NC, int R, int D>
 cudaError_t agg6_launch(const void* tmap, const AggArgs& a, cudaStream_t st) {
-  using Gm = Geom<NC, R>;
-  const size_t smem = (size_t)Gm::FLOATS * 4 + (2 + NVT) * Gm::K * sizeof(uint64_t);
-  cudaError_t e = cudaFuncSetAttribute(k_agg6<NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  using Gm = Geom<NC, R, D>;
+  using Ro = Roles<NC, D>;
+  const size_t smem = (size_t)Gm::FLOATS * 4 + (2 + Ro::NVT) * Gm::K * sizeof(uint64_t);
+  cudaError_t e = cudaFuncSetAttribute(k_agg6<NC, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int XSHIFT = (kWGroupPx - R % kWGroupPx) % kWGroupPx;
   dim3 grid((a.W + XSHIFT + TX - 1) / TX, (a.H + TY - 1) / TY);
-  k_agg6<NC, R><<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.L,
-                                             a.label_base, a.filtered_out, a.do_wta, a.first, a.last, a.best_cost,
-                                             a.best_label, a.labels_out, a.min_cost_out, a.keys_out, a.peer_keys,
-                                             a.rows_per_owner);
+  k_agg6<NC, R, D><<<grid, Ro::THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.L,
+                                                    a.label_base, a.filtered_out, a.do_wta, a.first, a.last,
+                                                    a.best_cost, a.best_label, a.labels_out, a.min_cost_out,
+                                                    a.keys_out, a.peer_keys, a.rows_per_owner);
   return cudaGetLastError();
 }
 
 }  // namespace v6a
+
+template <int NC, int D>
+inline cudaError_t agg6_r(int r, const void* tm, const AggArgs& a, cudaStream_t st) {
+  switch (r) {
+    case 1: return v6a::agg6_launch<NC, 1, D>(tm, a, st); case 2: return v6a::agg6_launch<NC, 2, D>(tm, a, st);
+    case 3: return v6a::agg6_launch<NC, 3, D>(tm, a, st); case 4: return v6a::agg6_launch<NC, 4, D>(tm, a, st);
+    case 5: return v6a::agg6_launch<NC, 5, D>(tm, a, st); case 6: return v6a::agg6_launch<NC, 6, D>(tm, a, st);
+    case 7: return v6a::agg6_launch<NC, 7, D>(tm, a, st); case 8: return v6a::agg6_launch<NC, 8, D>(tm, a, st);
+    case 9: return v6a::agg6_launch<NC, 9, D>(tm, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 }  // namespace hgf

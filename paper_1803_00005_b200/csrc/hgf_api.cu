@@ -341,7 +341,7 @@ cudaError_t launch_agg_chunk(hgf_ctx* h, const hgf::AggArgs& a, const void* tmap
       return hgf::launch_agg_v5(h->n, &h->tm_w5, &h->tm_ga5, h->W, h->H, h->r, a.L, a.label_base,
                                 hgf::kWGroupLabels, reinterpret_cast<unsigned long long*>(h->fkeys), a.filtered_out,
                                 h->stream);
-    if (h->v6agg) return hgf::launch_agg_v6(h->n, h->r, &h->tm_w6, a, h->stream);
+    if (h->v6agg) return hgf::launch_agg_v6(h->m, h->d, h->r, &h->tm_w6, a, h->stream);
     if (h->v3agg) return hgf::launch_agg_v3(h->n, h->r, h->tm_w, a, h->stream);
     return h->fast ? hgf::launch_agg_fast(h->n, a, h->stream) : hgf::launch_agg(h->n, a, h->stream);
   });

@@ -147,7 +147,8 @@ cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int 
 #define HGF_AGG6_TY 48
 #endif
 constexpr int kAgg6MaxN = 6, kAgg6TY = HGF_AGG6_TY;
-cudaError_t launch_agg_v6(int n, int r, const void* tm, const AggArgs& a, cudaStream_t st);
+// m, d: guide channels and degree (the owners of m <= 3 hold the raw channels; HGF_AGG6_KX=8 forces the planes).
+cudaError_t launch_agg_v6(int m, int d, int r, const void* tm, const AggArgs& a, cudaStream_t st);
 // keys[H][W] -> labels_out / min_cost_out / keys_out (each nullable) and, when peer_keys != null, a system-scope
 // 64-bit atomic MIN of every pixel's key into the row owner's buffer (the fused label-sharded merge).
 cudaError_t launch_keys_finalize(const int64_t* keys, int W, int H, int32_t* labels_out, float* min_cost_out,

@@ -602,27 +602,32 @@ def test_few_label_path_matches_main_path_and_oracle(monkeypatch, m, d, L, path)
     assert np.abs(a["filtered"] - b["filtered"]).max() <= 1e-4 * max(s_v, 1e-30)
 
 
-# k_agg6 (warp-specialised, per-plane pipeline) performs k_agg3's arithmetic in the same order: bit-identical
-# filtered costs, labels, minimum costs and keys, over ragged tiles, several 32-label groups, multi-chunk WTA
-# carries (small HGF_COEF_BUDGET_MB) and radii 1..9; k_agg6 also against the oracle on the smaller cases.
+# k_agg6 (warp-specialised, per-plane pipeline; 8-pixel owners holding the guidance planes or 16-pixel owners
+# holding the raw channels) performs k_agg3's arithmetic in the same order: bit-identical filtered costs, labels,
+# minimum costs and keys, over ragged tiles, several 32-label groups, multi-chunk WTA carries (small
+# HGF_COEF_BUDGET_MB), degrees 1..3 and radii 1..9; k_agg6 also against the oracle on the smaller cases.
 AGG6_CASES = [
-    # (W, H, L, m, d, r, budget MB)
-    (208, 72, 40, 3, 2, 9, None),
-    (301, 101, 70, 3, 2, 9, "1"),
-    (77, 53, 5, 3, 2, 9, None),
-    (160, 97, 33, 1, 2, 4, None),
-    (96, 130, 12, 2, 3, 1, None),
-    (128, 64, 9, 6, 1, 7, None),
+    # (W, H, L, m, d, r, budget MB, owner width: "16" = raw-channel owners where m <= 3, "8" = HGF_AGG6_KX=8)
+    (208, 72, 40, 3, 2, 9, None, "16"),
+    (208, 72, 40, 3, 2, 9, None, "8"),
+    (301, 101, 70, 3, 2, 9, "1", "16"),
+    (77, 53, 5, 3, 2, 9, None, "16"),
+    (160, 97, 33, 1, 2, 4, None, "16"),
+    (96, 130, 12, 2, 3, 1, None, "16"),
+    (112, 80, 7, 3, 1, 6, None, "16"),
+    (128, 64, 9, 6, 1, 7, None, "8"),
 ]
 
 
-@pytest.mark.parametrize("W,H,L,m,d,r,budget", AGG6_CASES)
-def test_agg6_bit_identical_to_agg3(monkeypatch, W, H, L, m, d, r, budget):
+@pytest.mark.parametrize("W,H,L,m,d,r,budget,kx", AGG6_CASES)
+def test_agg6_bit_identical_to_agg3(monkeypatch, W, H, L, m, d, r, budget, kx):
     torch = _torch()
     scene = synth.make_stereo_scene(W, H, L, seed=W + L)
     I = np.ascontiguousarray(synth.smooth_guides(W, H, m, seed=W)) if m != 3 else scene.left
     g = torch.from_numpy(I).cuda()
     vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    if kx == "8":
+        monkeypatch.setenv("HGF_AGG6_KX", "8")
     if budget:
         monkeypatch.setenv("HGF_COEF_BUDGET_MB", budget)
     out = {}
