@@ -753,6 +753,35 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   SmallLMode sm(h, 1);
+  const char* fe = std::getenv("HGF_FILTER_FUSED");
+  const hgf::WLayout& wl = h->planar_now ? h->wlay_planar : h->wlay;
+  if (!wl.il && !(fe && fe[0] == '0') && h->n <= hgf::kStats4MaxN && 64 + 2 * h->r <= 128 &&
+      hgf::stats4_smem(h->n, h->r, 1) <= 200 * 1024) {
+    // one slice: the statistics pass also sums the slice's cost products and writes its coefficients (no
+    // statistics in HBM, no coefficient kernel), then the planar aggregation
+    cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
+      return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->gp_pitch, h->m, h->d, h->W, h->H, h->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
+    e = traced(h, HGF_KC_STATS, h->stream, [&] {
+      const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+      return hgf::launch_filter1(h->n, h->G, src, h->wbuf, wl, h->W, h->H, h->r, h->eps, h->mode, lam0, h->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(h, e, "fused statistics + coefficients");
+    hgf::AggArgs a{};
+    a.G = h->G;
+    a.wbuf = h->wbuf;
+    a.W = h->W; a.H = h->H; a.r = h->r; a.L = 1; a.pad = wl.pad; a.il = 0;
+    a.label_base = 0;
+    a.filtered_out = dst;
+    a.first = 1;
+    a.last = 1;
+    a.best_cost = h->best_cost;
+    a.best_label = h->best_label;
+    e = launch_agg_chunk(h, a);
+    if (e != cudaSuccess) return cuda_fail(h, e, "agg");
+    return HGF_OK;
+  }
   if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   return slices(h, guide, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
 }

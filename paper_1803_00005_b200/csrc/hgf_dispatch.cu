@@ -96,6 +96,18 @@ cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int gp_pit
     default: return cudaErrorInvalidValue;                                             \
   }
 
+cudaError_t launch_filter1(int n, const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r,
+                           double lam, int mode, float lam0f, cudaStream_t st) {
+  if (n > kStats4MaxN || 64 + 2 * r > 128 || stats4_smem(n, r, 1) > 200 * 1024) return cudaErrorInvalidValue;
+  switch (n) {
+#define F1(N) \
+  case N: return st4::filter1_impl<N>(G, P, wout, wo, W, H, r, lam, mode, lam0f, st);
+    F1(1) F1(2) F1(3) F1(4) F1(5) F1(6) F1(7) F1(8) F1(9)
+#undef F1
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
                          float lam0f, int y0, int y1, double* scratch3, cudaStream_t st) {
   const int TS = 16 + 2 * r;

@@ -77,6 +77,8 @@ namespace hgf {
 namespace st4 {
 template cudaError_t stats4_impl<HGF_N>(const float*, float*, int, int, int, double, int, int, float, int, int,
                                         cudaStream_t);
+template cudaError_t filter1_impl<HGF_N>(const float*, const float*, float*, WLayout, int, int, int, double, int,
+                                         float, cudaStream_t);
 }  // namespace st4
 }  // namespace hgf
 #endif

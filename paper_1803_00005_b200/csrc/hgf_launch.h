@@ -35,9 +35,14 @@ cudaError_t launch_poly_guidance(const float* I, float* G, float* Gp, int gp_pit
 // Rows [y0, y1) of the statistics (the k_stats2 path; the v1 kernel only supports the full image).
 // scratch3: (stats3_scratch_planes(n)) * H * W doubles, or null (k_stats3 is used for n >= kStats3MinN).
 constexpr int kStats4MaxN = 9;      // k_stats4 (row-marching) up to here, when its rows fit SMEM
-inline size_t stats4_smem(int n, int r) {   // = st4::smem_bytes
-  return (size_t)2 * ((n + 1) * (n + 2) / 2 - 1) * (((64 + 2 * r) | 1) + 65) * sizeof(double);
+inline size_t stats4_smem(int n, int r, int lp = 0) {   // = st4::smem_bytes
+  return (size_t)2 * ((n + 1) * (n + 2) / 2 - 1 + lp * (n + 1)) * (((64 + 2 * r) | 1) + 65) * sizeof(double);
 }
+// hgf_filter's fused single-slice pass (k_stats4<n, 1>): guidance G + cost slice P -> the slice's coefficients w
+// in the planar layout wo, the statistics never stored; n <= kStats4MaxN, 64 + 2r <= 128, stats4_smem(n, r, 1)
+// within 200 KB (else cudaErrorInvalidValue).
+cudaError_t launch_filter1(int n, const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r,
+                           double lam, int mode, float lam0f, cudaStream_t st);
 constexpr int kStats3MinN = 18;     // always k_stats3 from here; below only when k_stats2 does not fit
 inline long long stats3_scratch_planes(int n) { return (long long)(n + 1) * (n + 2) / 2 - 1 + 32; }
 cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
@@ -173,5 +178,8 @@ namespace st4 {
 template <int NC>
 cudaError_t stats4_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
                         int y0, int y1, cudaStream_t st);
+template <int NC>
+cudaError_t filter1_impl(const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r, double lam,
+                         int mode, float lam0f, cudaStream_t st);
 }  // namespace st4
 }  // namespace hgf

@@ -10,15 +10,14 @@
 
 namespace hgf {
 
-// g: the NPAIR = (n+1)(n+2)/2 - 1 Gram sums of pixel p, pairs (a, b), a <= b, enumerated row-major over the
-// upper triangle with (0, 0) skipped.  Writes the record (aos) or the planar statistics of pixel p.
-template <int NC, int MODE>
-__device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC + 2) / 2 - 1], double N, double lam,
-                                               int aos, float lam0f, float* __restrict__ stats, long long p,
-                                               long long HW) {
+// g: the Gram sums of pixel p, pairs (a, b), a <= b, enumerated row-major over the upper triangle with (0, 0)
+// skipped (the first (n+1)(n+2)/2 - 1 entries; NG may be larger: k_stats4's fused single-slice variant appends the
+// cost sums).  Gm = the (centred, GF) Gram matrix, al = alpha of the Prop-1 recursion.
+template <int NC, int MODE, int NG>
+__device__ __forceinline__ void gram_alpha(const double (&g)[NG], double N, double lam, double (&Gm)[NC + 1][NC + 1],
+                                           double (&al)[NC + 1][NC + 1]) {
   constexpr int mode = MODE;   // compile-time: no runtime mode tests in the unrolled recursion
   constexpr int K = NC + 1;
-  double Gm[K][K];
 #pragma unroll
   for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -40,7 +39,6 @@ __device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC 
         Gm[b][a] = Gm[a][b];
       }
   }
-  double al[K][K];
 #pragma unroll
   for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -74,6 +72,17 @@ __device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC 
     }
     al[k][k] = inv_lam * inv_lam * gam;
   }
+}
+
+// Writes the record (aos) or the planar statistics of pixel p.
+template <int NC, int MODE>
+__device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC + 2) / 2 - 1], double N, double lam,
+                                               int aos, float lam0f, float* __restrict__ stats, long long p,
+                                               long long HW) {
+  constexpr int mode = MODE;
+  constexpr int K = NC + 1;
+  double Gm[K][K], al[K][K];
+  gram_alpha<NC, MODE>(g, N, lam, Gm, al);
   const double inv_den = 1.0 / ((mode == 0) ? (lam + N) : N);   // one division, then products
   if (aos) {
     constexpr int REC = stats_aos_floats(NC);
@@ -100,6 +109,36 @@ __device__ __forceinline__ void stats_finish_m(const double (&g)[(NC + 1) * (NC 
     for (int b = a; b < K; ++b) stats[(long long)(s++) * HW + p] = (float)(-lam * al[a][b]);
 #pragma unroll
   for (int a = 1; a < K; ++a) stats[(long long)(s++) * HW + p] = (float)(Gm[0][a] * inv_den);
+}
+
+// Single-slice end (k_stats4's fused variant, hgf_filter): g additionally holds, after the Gram pairs, the cost sums
+// S_a = B(G_a p) for a = 0..n (G_0 = ones, so S_0 = B(p)).  The coefficients of the slice are those k_coef* form
+// from the stored statistics (w = P'(S - nu S_0), w_0 = kappa S_0 - nu^T w, P' = -lambda alpha,
+// nu = B(G)/(lambda_0 + N) (HGF) or B(G)/N (GF), kappa = 1/(lambda_0 + N)), here in float64 straight from the
+// float64 sums, written as float32 planes w_0..w_n at wl[k * plane].
+template <int NC, int MODE, int NG>
+__device__ __forceinline__ void filter_finish_m(const double (&g)[NG], double N, double lam, float lam0f,
+                                                float* __restrict__ wl, long long plane) {
+  constexpr int K = NC + 1;
+  constexpr int NPAIR = K * (K + 1) / 2 - 1;
+  static_assert(NG == NPAIR + K, "Gram pairs + cost sums");
+  double Gm[K][K], al[K][K];
+  gram_alpha<NC, MODE>(g, N, lam, Gm, al);
+  const double inv_den = 1.0 / ((MODE == 0) ? (lam + N) : N);
+  const double S0 = g[NPAIR];
+  double c[K];
+#pragma unroll
+  for (int a = 1; a < K; ++a) c[a] = g[NPAIR + a] - Gm[0][a] * inv_den * S0;
+  double w0 = S0 / ((double)lam0f + N);
+#pragma unroll
+  for (int a = 1; a < K; ++a) {
+    double t = 0.0;
+#pragma unroll
+    for (int b = 1; b < K; ++b) t += (-lam * al[a][b]) * c[b];
+    w0 -= Gm[0][a] * inv_den * t;
+    wl[a * plane] = (float)t;
+  }
+  wl[0] = (float)w0;
 }
 
 template <int NC>

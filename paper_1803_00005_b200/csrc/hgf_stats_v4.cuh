@@ -37,20 +37,27 @@ constexpr int NSEG = TX / HSEG;
 constexpr int TXP = TX + 1;        // hs row pitch (doubles, odd)
 
 __host__ __device__ constexpr int npair(int n) { return (n + 1) * (n + 2) / 2 - 1; }
+// sums per pixel: the Gram pairs, plus (LP = 1, the fused single-slice variant) the cost sums B(G_a p), a = 0..n
+__host__ __device__ constexpr int nsums(int n, int lp) { return npair(n) + lp * (n + 1); }
 __host__ __device__ inline int vx_pitch(int r) { return (TX + 2 * r) | 1; }
-__host__ __device__ inline size_t smem_bytes(int NC, int r) {
-  return (size_t)RB * npair(NC) * (vx_pitch(r) + TXP) * sizeof(double);
+__host__ __device__ inline size_t smem_bytes(int NC, int r, int lp = 0) {
+  return (size_t)RB * nsums(NC, lp) * (vx_pitch(r) + TXP) * sizeof(double);
 }
 
 // Rows [yb0, yb1).  CTA (bx, by) owns columns [bx*TX, +TX) and the absolute band of rows
 // [(yb0/BH + by)*BH, +BH), BH a function of (W, H) only: every row's running sums have the same history
 // whichever row range is requested, so row-sharded statistics are bit-identical to the full pass.
-template <int NC>
+// LP = 1 (hgf_filter, one slice p): the cost is an extra channel whose products with G_0..G_n are summed with the
+// Gram pairs, and the R phase writes the slice's coefficients w (planar, wl) instead of the statistics
+// (filter_finish_m): the statistics never reach HBM and no coefficient kernel runs.
+template <int NC, int LP>
 __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G, float* __restrict__ stats, int W,
                                                     int H, int r, double lam, int mode, int aos, float lam0f,
-                                                    int yb0, int yb1, int BH) {
+                                                    int yb0, int yb1, int BH, const float* __restrict__ P,
+                                                    float* __restrict__ wout, WLayout wo) {
   constexpr int K = NC + 1;
-  constexpr int NPAIR = npair(NC);
+  constexpr int NG = npair(NC);                 // Gram pairs
+  constexpr int NPAIR = nsums(NC, LP);          // all running sums
   extern __shared__ __align__(16) double sd[];
   const int VXP = vx_pitch(r);
   double* vs = sd;                             // [RB][NPAIR][VXP]
@@ -66,12 +73,13 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
   const int vx = x0 - r + tid;
   const bool vcol = tid < CX;
   const bool xin = vcol && vx >= 0 && vx < W;
-  auto load_row = [&](int yy, float (&v)[K]) {
+  auto load_row = [&](int yy, float (&v)[K + LP]) {
     const bool in = xin && yy >= 0 && yy < H;
     v[0] = in ? 1.0f : 0.0f;
     const float* src = G + (long long)yy * W + vx;
 #pragma unroll
     for (int k = 1; k < K; ++k) v[k] = in ? __ldg(src + (k - 1) * HW) : 0.0f;
+    if (LP) v[K] = in ? __ldg(P + (long long)yy * W + vx) : 0.0f;
   };
 
   // warm-up: the window of output row Y0 - 1 (rows Y0 - 1 - r .. Y0 - 1 + r), kept in vs[RB - 1]
@@ -80,7 +88,7 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
 #pragma unroll
     for (int q = 0; q < NPAIR; ++q) acc[q] = 0.0;
     for (int yy = Y0 - 1 - r; yy <= Y0 - 1 + r; ++yy) {
-      float e[K];
+      float e[K + LP];
       load_row(yy, e);
       int q = 0;
 #pragma unroll
@@ -91,6 +99,10 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
           acc[q] = fma((double)e[a], (double)e[b], acc[q]);
           ++q;
         }
+      if constexpr (LP == 1) {
+#pragma unroll
+        for (int a = 0; a < K; ++a) acc[NG + a] = fma((double)e[a], (double)e[K], acc[NG + a]);
+      }
     }
     double* dst = vs + (RB - 1) * NPAIR * VXP + tid;
 #pragma unroll
@@ -100,7 +112,7 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
   for (int yb = Y0; yb < Z1; yb += RB) {
     // ---- V phase: rows yb .. yb + RB - 1
     if (vcol) {
-      float e[RB][K], l[RB][K];
+      float e[RB][K + LP], l[RB][K + LP];
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         load_row(yb + rb + r, e[rb]);
@@ -121,6 +133,11 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
             acc[q] = fma((double)e[rb][a], (double)e[rb][b], fma(-(double)l[rb][a], (double)l[rb][b], acc[q]));
             ++q;
           }
+        if constexpr (LP == 1) {
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+            acc[NG + a] = fma((double)e[rb][a], (double)e[rb][K], fma(-(double)l[rb][a], (double)l[rb][K], acc[NG + a]));
+        }
         double* dst = vs + rb * NPAIR * VXP + tid;
 #pragma unroll
         for (int q2 = 0; q2 < NPAIR; ++q2) dst[q2 * VXP] = acc[q2];
@@ -153,20 +170,26 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
 #pragma unroll
         for (int q = 0; q < NPAIR; ++q) g[q] = src[q * TXP];
         const double N = (double)window_count(gy, gx, H, W, r);
-        stats_finish<NC>(g, N, lam, mode, aos, lam0f, stats, (long long)gy * W + gx, HW);
+        if constexpr (LP == 1) {
+          float* wl = wout + wo.origin + (long long)gy * wo.pitch + gx;
+          if (mode == 0) filter_finish_m<NC, 0>(g, N, lam, lam0f, wl, wo.plane);
+          else filter_finish_m<NC, 1>(g, N, lam, lam0f, wl, wo.plane);
+        } else {
+          stats_finish<NC>(g, N, lam, mode, aos, lam0f, stats, (long long)gy * W + gx, HW);
+        }
       }
     }
     // the next V phase overwrites vs only (hs is rewritten after the next barrier)
   }
 }
 
-template <int NC>
-cudaError_t stats4_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
-                        int y0, int y1, cudaStream_t st) {
+template <int NC, int LP>
+cudaError_t stats4_launch(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
+                          float lam0f, int y0, int y1, const float* P, float* wout, WLayout wo, cudaStream_t st) {
   if (aos && NC > kCoef3MaxN) return cudaErrorInvalidValue;
   if (TX + 2 * r > THREADS) return cudaErrorInvalidValue;
-  const size_t smem = smem_bytes(NC, r);
-  cudaError_t e = cudaFuncSetAttribute(k_stats4<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = smem_bytes(NC, r, LP);
+  cudaError_t e = cudaFuncSetAttribute(k_stats4<NC, LP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (y0 >= y1) return cudaSuccess;
   // band height from (W, H) only (see k_stats4): >= ~6 CTAs per SM over the whole image where it allows,
@@ -175,8 +198,21 @@ cudaError_t stats4_impl(const float* G, float* stats, int W, int H, int r, doubl
   int BH = 128;
   while (BH > 16 && (long long)strips * ((H + BH - 1) / BH) < 6 * 148) BH /= 2;
   dim3 grid(strips, (y1 + BH - 1) / BH - y0 / BH);
-  k_stats4<NC><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH);
+  k_stats4<NC, LP><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout, wo);
   return cudaGetLastError();
+}
+
+template <int NC>
+cudaError_t stats4_impl(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
+                        int y0, int y1, cudaStream_t st) {
+  return stats4_launch<NC, 0>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, nullptr, nullptr, WLayout{}, st);
+}
+
+// hgf_filter's fused single-slice pass: guidance G, cost slice P -> coefficients w (planar layout wo) of all rows.
+template <int NC>
+cudaError_t filter1_impl(const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r, double lam,
+                         int mode, float lam0f, cudaStream_t st) {
+  return stats4_launch<NC, 1>(G, nullptr, W, H, r, lam, mode, 0, lam0f, 0, H, P, wout, wo, st);
 }
 
 }  // namespace st4

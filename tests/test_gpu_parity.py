@@ -132,6 +132,60 @@ def test_filter_entry_point():
     h.close()
 
 
+# hgf_filter's fused single-slice pass (k_stats4<n, 1>: the statistics pass also sums the slice's cost products and
+# writes its coefficients, then the planar aggregation): ragged frames, degrees 1..3, n up to 9, both modes, against
+# the oracle and against the unfused path (HGF_FILTER_FUSED=0: statistics -> k_coef2 -> aggregation).
+FILTER1_CASES = [
+    # (W, H, m, d, r, mode)
+    (133, 71, 3, 2, 9, "hgf"),
+    (133, 71, 3, 2, 9, "gf"),
+    (96, 50, 1, 1, 4, "hgf"),
+    (70, 45, 3, 3, 7, "gf"),
+    (64, 97, 2, 2, 1, "hgf"),
+    (128, 40, 6, 1, 9, "hgf"),
+]
+
+
+@pytest.mark.parametrize("W,H,m,d,r,mode", FILTER1_CASES)
+def test_filter_fused_single_slice(monkeypatch, W, H, m, d, r, mode):
+    torch = _torch()
+    I = synth.smooth_guides(W, H, m, seed=W + r)
+    scene = synth.make_stereo_scene(W, H, 16, seed=H)
+    Y = np.ascontiguousarray(synth.stereo_cost_volume_np(scene, 16, 5, 6)[0])
+    g, y = torch.from_numpy(I).cuda(), torch.from_numpy(Y).cuda()
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("HGF_FILTER_FUSED", fused)
+        h = _hgf(W, H, m, d, r, 0.05, mode)
+        out[fused] = h.filter(g, y)
+        torch.cuda.synchronize()
+        launches = h.last_launch_count
+        h.close()
+        if fused == "1":
+            assert launches == 3, launches        # guidance, fused statistics + coefficients, aggregation
+    s_v = float(np.abs(Y).max())
+    Z = O.hgf_filter(I, Y, 0.05, r, d, mode=mode)
+    check_z(out["1"].cpu().numpy(), Z, s_v)
+    check_z(out["0"].cpu().numpy(), Z, s_v)
+
+
+def test_c5_full_frame_fused_filter():
+    """BASELINE config 5 at n = 6, r = 9 (RGB, degree 2) in full: every pixel of the 1920x1080 single-slice
+    hgf_filter (fused path) against the oracle."""
+    torch = _torch()
+    c = synth.config("C5")
+    W, H, lam = c["W"], c["H"], c["lam"]
+    I = synth.smooth_guides(W, H, 3, seed=5)
+    scene = synth.make_stereo_scene(W, H, 64, seed=5)
+    Y = np.ascontiguousarray(synth.stereo_cost_volume_np(scene, 64, 20, 21)[0])
+    h = _hgf(W, H, 3, 2, 9, lam)
+    dst = h.filter(torch.from_numpy(I).cuda(), torch.from_numpy(Y).cuda())
+    torch.cuda.synchronize()
+    assert h.last_launch_count == 3
+    h.close()
+    check_z(dst.cpu().numpy(), O.hgf_filter(I, Y, lam, 9, 2), float(np.abs(Y).max()))
+
+
 def test_deterministic_and_label_offset_and_permutation():
     I, V = synth.iid_volume(50, 40, 6, 3, seed=5)
     a = _run(I, V, 2, 4, 0.05)
