@@ -9,19 +9,18 @@
 // per SM it spends a third of its time in the four CTA barriers per slice (vertical pass on 16 warps with 21
 // warp-items of work, horizontal pass on 12 owner warps) and waiting for the next plane group's TMA, which it
 // can only issue half a slice ahead.  Here:
-//   * every plane of the slice has its own 1 KB-aligned buffer and three mbarriers: full (TMA landed), vdone
-//     (vertical sums written), hdone (owners finished reading);
-//   * warp 15 lane 0 (producer) refills plane k for slice l + 1 as soon as the owners release it, i.e. K - 1
-//     plane-steps before it is needed (k_agg3: one plane group);
-//   * warps 12..14 (96 threads = the tile's 96 swizzled columns) do the in-place vertical window sums of plane
-//     k, then arrive on vdone[k];
-//   * warps 0..11 (owners: row x 8 pixels, k_agg3's conflict-free swizzled mapping) wait on vdone[k], do the
-//     horizontal sums, Z and (after the last plane) the WTA, then arrive on hdone[k].
-// The vertical warps run ahead of the owners by up to a slice, so both passes keep the LSU busy without CTA
-// barriers.  vdone / hdone complete once per slice (phase parity l & 1).  With two vertical teams (alternate
-// plane-steps s = lK + k) plane k's TMA for slice l signals full[k][l % 2], which only one team waits on, in slice
-// order (parity (l / 2) & 1): a parity wait must never run two phases ahead of the barrier, which a single
-// full[k] shared by both teams would allow.
+//   * the coefficient planes arrive one TMA box each (plane-step s = lK + k: plane k of slice l) into a ring of NB
+//     1 KB-aligned slots (as many as shared memory holds: 9 at r = 9, NB >= K), slot s % NB with three mbarriers:
+//     full (TMA landed), vdone (vertical sums written), hdone (owners finished reading); each completes once per
+//     NB plane-steps (phase parity (s / NB) & 1);
+//   * the last warp's lane 0 (producer) refills a slot as soon as the owners release it, NB - 1 plane-steps before
+//     it is needed (k_agg3: one plane group, half a slice);
+//   * 3 vertical warps (96 threads = the tile's 96 swizzled columns) do the in-place vertical window sums of a
+//     plane, then arrive on vdone;
+//   * owner warps (rows x 8 or 16 pixels, conflict-free swizzled mappings) wait on vdone, do the horizontal sums,
+//     Z and (after the last plane of a slice) the WTA, then arrive on hdone.
+// The vertical warps run up to NB - 1 plane-steps ahead of the owners, so both passes keep the LSU busy without CTA
+// barriers; that slack is what pays (cutting it to two plane-steps cost 18 %, growing it from K - 1 = 6 to 8: -2 %).
 #pragma once
 #include <cuda.h>
 
@@ -33,14 +32,9 @@
 namespace hgf {
 namespace v6a {
 
-// Tile height (HGF_AGG6_TY, = kAgg6TY): 48 rows -> 12 owner warps and one vertical team of 3 warps; 36 rows -> 9
-// owner warps and two vertical teams (alternate plane-steps), for 1.5x instead of 1.375x vertical halo: measured
-// the same C4 time (17.05 vs 17.0 ms per frame), so 48 (bit-identical to k_agg3's 48-row tiles).
-#ifndef HGF_AGG6_TY
-#define HGF_AGG6_TY 48
-#endif
-constexpr int TX = 64, TY = HGF_AGG6_TY;
-constexpr int NVW = 3;                     // warps per vertical team (one column each of the 96-column tile)
+// Tile height 48 (= kAgg6TY; 36-row tiles with two vertical teams measured the same C4 time).
+constexpr int TX = 64, TY = 48;
+constexpr int NVW = 3;                     // vertical warps (one column each of the 96-column tile)
 static_assert(TY == kAgg6TY, "host box height");
 static_assert(kWGroupPx == 16, "64-byte swizzle (16-pixel groups)");
 
@@ -55,9 +49,9 @@ struct Roles {
   static constexpr int KX = D == 0 ? 8 : 16, NSEG = TX / KX;
   static constexpr int NOWN = TY * NSEG;             // owner threads = warps [0, NOWN / 32)
   static constexpr int THREADS = D == 0 ? 512 : NOWN + 32 * NVW + 32;   // the last warp is the TMA producer
-  static constexpr int NVT = (THREADS / 32 - 1 - NOWN / 32) / NVW;     // vertical teams
+
   static constexpr int MG = D == 0 ? NC : NC / (D > 0 ? D : 1);    // guide values held per owner pixel
-  static_assert(NOWN % 32 == 0 && NVT >= 1 && NOWN + 32 * NVW * NVT + 32 == THREADS, "warp roles");
+  static_assert(NOWN % 32 == 0 && NOWN + 32 * NVW + 32 == THREADS, "warp roles");
   static_assert(D == 0 || (NC % (D > 0 ? D : 1) == 0 && NC / (D > 0 ? D : 1) <= 3), "raw-channel owners: m <= 3");
   // registers per thread: each SM sub-partition holds 16384, and takes up to ceil(warps / 4) of the CTA's warps
   static constexpr int MAXREG = (16384 / (32 * ((THREADS / 32 + 3) / 4))) / 8 * 8 > 255
@@ -74,7 +68,11 @@ struct Geom {
   static constexpr int BY = TY + 2 * R;
   static constexpr int PLANE = BX * BY;                        // floats per plane tile
   static constexpr int PSTRIDE = (PLANE + 255) / 256 * 256;    // 1 KB-aligned plane buffers
-  static constexpr int FLOATS = K * PSTRIDE;
+  // ring slots: as many plane buffers as fit next to the barriers and the 1 KB static reservation (<= 16)
+  static constexpr int NBFIT = (227 * 1024 - 1024 - 16 * 3 * 8) / (PSTRIDE * 4);
+  static constexpr int NB = NBFIT > 16 ? 16 : NBFIT;
+  static_assert(NB >= K, "one slice of planes in flight");
+  static constexpr int FLOATS = NB * PSTRIDE;
   static constexpr int NV4 = (KX + 2 * R + 3) / 4;
   static_assert(BX == 32 * NVW, "one vertical thread per tile column");
   static_assert(KX * (NSEG - 1) + 4 * NV4 <= BX, "owner loads stay inside the row");
@@ -100,11 +98,11 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
   using Gm = Geom<NC, R, D>;
   using Ro = Roles<NC, D>;
   constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PSTRIDE = Gm::PSTRIDE, NV4 = Gm::NV4, KX = Gm::KX;
-  constexpr int NOWN = Ro::NOWN, THREADS = Ro::THREADS, NVT = Ro::NVT, MG = Ro::MG;
+  constexpr int NOWN = Ro::NOWN, THREADS = Ro::THREADS, MG = Ro::MG, NB = Gm::NB;
   extern __shared__ __align__(1024) float buf[];
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + Gm::FLOATS);
-  uint64_t* vdone = full + K * NVT;   // full[k * NVT + l % NVT]: see below
-  uint64_t* hdone = vdone + K;
+  uint64_t* vdone = full + NB;        // per ring slot: TMA landed / vertical sums written / owners released
+  uint64_t* hdone = vdone + NB;
   const int tid = threadIdx.x, wq = tid >> 5, ln = tid & 31;
   // tile origin shifted so the TMA x coordinate x0 - R is a whole 16-pixel group (unaligned x traps); grouped
   // tile order (GY tiles down a column) so the CTAs resident at once share their R-halos through L2 (k_agg3)
@@ -125,10 +123,10 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
   const long long HW = (long long)H * W;
 
   if (tid == 0) {
-    for (int k = 0; k < K; ++k) {
-      for (int t = 0; t < NVT; ++t) mbar_init(&full[k * NVT + t], 1);
-      mbar_init(&vdone[k], NVW);
-      mbar_init(&hdone[k], NOWN / 32);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&vdone[b], NVW);
+      mbar_init(&hdone[b], NOWN / 32);
     }
     cuda::ptx::fence_mbarrier_init(cuda::ptx::sem_release, cuda::ptx::scope_cluster);
   }
@@ -139,34 +137,33 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     // ---- producer: plane k of slice l into buffer k once the owners have released slice l - 1's plane k
     if (ln != 0) return;
     for (int s = 0; s < S; ++s) {
-      const int l = s / K, k = s - l * K;
-      if (l > 0) {
-        mbar_wait(&hdone[k], (l - 1) & 1);
+      const int l = s / K, k = s - l * K, b = s % NB;
+      if (s >= NB) {
+        mbar_wait(&hdone[b], (s / NB - 1) & 1);
         cuda::ptx::fence_proxy_async(cuda::ptx::space_shared);
       }
       cuda::ptx::mbarrier_arrive_expect_tx(cuda::ptx::sem_release, cuda::ptx::scope_cta, cuda::ptx::space_shared,
-                                           &full[k * NVT + l % NVT], (uint32_t)(Gm::PLANE * 4));
+                                           &full[b], (uint32_t)(Gm::PLANE * 4));
       const int32_t c[5] = {0, l % kWGroupLabels, tx0 / kWGroupPx, ty0, (l / kWGroupLabels) * K + k};
-      cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, buf + k * PSTRIDE, &tm, c,
-                                      &full[k * NVT + l % NVT]);
+      cuda::ptx::cp_async_bulk_tensor(cuda::ptx::space_cluster, cuda::ptx::space_global, buf + b * PSTRIDE, &tm, c,
+                                      &full[b]);
     }
     return;
   }
 
   if (wq >= NOWN / 32) {
-    const int team = (wq - NOWN / 32) / NVW;
     // ---- vertical warps: column c of every plane, in place: rows [0, TY) <- sum of rows [y, y + 2R].  The whole
     // column is loaded before the first sum (one shared-memory round trip per plane); same summation order as
     // k_agg3, so the two kernels are bit-identical.  (Two independent half-column chains were measured: no gain.)
-    const int c = tid - NOWN - 32 * NVW * team;
+    const int c = tid - NOWN;
     // swizzled address of row y: (c ^ m(y)) + y*BX, the XOR mask depending only on y mod 4 (BX = 96 floats)
     int fb[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) fb[j] = c ^ ((((c >> 5) + j * (BX / 32)) & 3) << 2);
-    for (int s = team; s < S; s += NVT) {
-      const int l = s / K, k = s - l * K;
-      float* lb = buf + k * PSTRIDE;
-      mbar_wait(&full[k * NVT + l % NVT], (l / NVT) & 1);
+    for (int s = 0; s < S; ++s) {
+      const int b = s % NB;
+      float* lb = buf + b * PSTRIDE;
+      mbar_wait(&full[b], (s / NB) & 1);
       if (c < Gm::WX) {
         float col[BY];
 #pragma unroll
@@ -182,7 +179,7 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
         }
       }
       __syncwarp();
-      if (ln == 0) mbar_arrive(&vdone[k]);
+      if (ln == 0) mbar_arrive(&vdone[b]);
     }
     return;
   }
@@ -234,8 +231,9 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
   for (int l = 0; l < L; ++l) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const float* lb = buf + k * PSTRIDE;
-      mbar_wait(&vdone[k], l & 1);
+      const int sg = l * K + k, b = sg % NB;
+      const float* lb = buf + b * PSTRIDE;
+      mbar_wait(&vdone[b], (sg / NB) & 1);
       float f[4 * NV4];
 #pragma unroll
       for (int q = 0; q < NV4; ++q) {
@@ -257,7 +255,7 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
       }
       // release the plane once its loaded values have been consumed
       __syncwarp();
-      if (ln == 0) mbar_arrive(&hdone[k]);
+      if (ln == 0) mbar_arrive(&hdone[b]);
     }
 #pragma unroll
     for (int s = 0; s < KX; ++s) {
@@ -300,7 +298,7 @@ template <int NC, int R, int D>
 cudaError_t agg6_launch(const void* tmap, const AggArgs& a, cudaStream_t st) {
   using Gm = Geom<NC, R, D>;
   using Ro = Roles<NC, D>;
-  const size_t smem = (size_t)Gm::FLOATS * 4 + (2 + Ro::NVT) * Gm::K * sizeof(uint64_t);
+  const size_t smem = (size_t)Gm::FLOATS * 4 + 3 * Gm::NB * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(k_agg6<NC, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int XSHIFT = (kWGroupPx - R % kWGroupPx) % kWGroupPx;

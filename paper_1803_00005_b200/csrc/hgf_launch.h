@@ -148,10 +148,7 @@ cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int 
 // Warp-specialised aggregation (hgf_agg_v6.cuh, instantiated in hgf_agg6.cu): 64 x kAgg6TY tiles on the
 // label-interleaved layout, n <= 6, r <= 9; tm: rank-5 map over the coefficient buffer with a one-plane box
 // (16, 1, ceil32(64 + 2r) / 16, kAgg6TY + 2r, 1), 64-byte swizzle.  Same AggArgs contract as k_agg3 (a.il == 1).
-#ifndef HGF_AGG6_TY
-#define HGF_AGG6_TY 48
-#endif
-constexpr int kAgg6MaxN = 6, kAgg6TY = HGF_AGG6_TY;
+constexpr int kAgg6MaxN = 6, kAgg6TY = 48;
 // m, d: guide channels and degree (the owners of m <= 3 hold the raw channels; HGF_AGG6_KX=8 forces the planes).
 cudaError_t launch_agg_v6(int m, int d, int r, const void* tm, const AggArgs& a, cudaStream_t st);
 // keys[H][W] -> labels_out / min_cost_out / keys_out (each nullable) and, when peer_keys != null, a system-scope
