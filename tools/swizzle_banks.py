@@ -1,6 +1,7 @@
-"""Shared-memory bank check for k_agg3's tile under the 64-byte (IL) / 32-byte (IL8, HGF_WG8) TMA swizzle and the planar
-odd-pitch tile: counts wavefronts per quarter-warp for the owner LDS.128 pattern and ways per warp for the
-vertical pass.  Usage: python tools/swizzle_banks.py [R]
+"""Shared-memory bank check for k_agg3's / k_agg6's tile under the 64-byte (IL) / 32-byte (IL8, HGF_WG8) TMA swizzle
+and the planar odd-pitch tile: counts wavefronts per quarter-warp for the owner LDS.128 pattern and ways per warp for
+the vertical pass; k_agg6's 16-pixel owners (4 rows x 2 segments per quarter-warp, 8 rows per warp) as well.
+Usage: python tools/swizzle_banks.py [R]
 """
 import sys
 
@@ -71,5 +72,36 @@ def main():
               f"(ideal 4); vertical pass worst {vworst}-way")
 
 
+def owner16(ln, wq):
+    """k_agg6 16-pixel owners (D >= 1): row, segment of lane ln in owner warp wq."""
+    return (ln & 3) + 4 * (ln >> 4) + 8 * wq, (ln >> 2) & 3
+
+
+def lds_wavefronts(addrs, width):
+    """LDS.128 is served per quarter-warp (8 lanes), LDS.64 per half-warp (16 lanes)."""
+    grp = 8 if width == 4 else 16
+    tot = 0
+    for g0 in range(0, 32, grp):
+        banks = {}
+        for a in addrs[g0:g0 + grp]:
+            for j in range(width):
+                banks.setdefault((a + j) % 32, set()).add((a + j) // 32)
+        tot += max(len(v) for v in banks.values())
+    return tot
+
+
+def main16(R):
+    BX, nf = 96, 16 + 2 * R
+    res = set()
+    for wq in range(6):
+        for q in range((nf + 3) // 4):
+            width = 4 if 4 * q + 4 <= nf else nf - 4 * q
+            addrs = [swz(owner16(ln, wq)[0] * BX + owner16(ln, wq)[1] * 16 + 4 * q) for ln in range(32)]
+            res.add((width, lds_wavefronts(addrs, width)))
+    print(f"R={R} k_agg6 16-pixel owners: (load width in floats, wavefronts per warp load) = {sorted(res)} "
+          f"(ideal: 4 for 128-bit loads)")
+
+
 if __name__ == "__main__":
     main()
+    main16(int(sys.argv[1]) if len(sys.argv) > 1 else 9)
