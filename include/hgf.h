@@ -260,8 +260,10 @@ HGF_API hgf_status hgf_profile_read(hgf_handle h, double* ms, int* counts, int n
 HGF_API int hgf_last_launch_count(hgf_handle h);
 
 /* The slice-kernel pair this handle runs, fixed at create time from (W, H, n_guide, poly_degree, radius)
- * and the HGF_* selection variables: "coef5+agg3" (default for m <= 3, d <= 3, n <= 6, r <= 9, W % 4 == 0),
- * "coef5+agg5" (opt-in), "coef3+agg3", "coef4+agg3", "coef2+agg3", "coef2+agg2", "coef1+agg1".  Static string; NULL handle -> "". */
+ * and the HGF_* selection variables: "coef5+agg6" (default for m <= 3, d <= 3, n <= 6, r <= 9, W % 4 == 0 or
+ * d == 2), "coef3+agg6" (n <= 6 otherwise, W % 4 == 0), "coef5+agg3" / "coef3+agg3" (HGF_AGG6=0), "coef5+agg5"
+ * (opt-in), "coef4+agg3", "coef2+agg3", "coef2+agg2", "coef1+agg1".  Few-label calls (L <= 2, hgf_filter) run
+ * planar paths whatever this reports (hgf_filter: the fused single-slice pass).  Static string; NULL handle -> "". */
 HGF_API const char* hgf_kernel_path(hgf_handle h);
 
 /* Static description of a status code. */

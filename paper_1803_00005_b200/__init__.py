@@ -157,7 +157,7 @@ class HGF:
 
     @property
     def kernel_path(self):
-        """The slice kernels this handle runs (hgf_kernel_path), e.g. "coef5+agg3"."""
+        """The slice kernels this handle runs (hgf_kernel_path), e.g. "coef5+agg6"."""
         return lib().hgf_kernel_path(self._h).decode()
 
     # ------------------------------------------------------------------ API (names as in hgf.h)
