@@ -50,11 +50,14 @@ __host__ __device__ inline size_t smem_bytes(int NC, int r, int lp = 0) {
 // LP = 1 (hgf_filter, one slice p): the cost is an extra channel whose products with G_0..G_n are summed with the
 // Gram pairs, and the R phase writes the slice's coefficients w (planar, wl) instead of the statistics
 // (filter_finish_m): the statistics never reach HBM and no coefficient kernel runs.
-template <int NC, int LP>
+// RT > 0: the radius as a compile-time constant (the H phase's window loops unroll and their shared loads issue
+// ahead of the dependent adds); RT = 0: r at run time.
+template <int NC, int LP, int RT>
 __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G, float* __restrict__ stats, int W,
-                                                    int H, int r, double lam, int mode, int aos, float lam0f,
+                                                    int H, int r_arg, double lam, int mode, int aos, float lam0f,
                                                     int yb0, int yb1, int BH, const float* __restrict__ P,
                                                     float* __restrict__ wout, WLayout wo) {
+  const int r = RT > 0 ? RT : r_arg;
   constexpr int K = NC + 1;
   constexpr int NG = npair(NC);                 // Gram pairs
   constexpr int NPAIR = nsums(NC, LP);          // all running sums
@@ -183,13 +186,13 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
   }
 }
 
-template <int NC, int LP>
-cudaError_t stats4_launch(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
+template <int NC, int LP, int RT>
+cudaError_t stats4_launch_r(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
                           float lam0f, int y0, int y1, const float* P, float* wout, WLayout wo, cudaStream_t st) {
   if (aos && NC > kCoef3MaxN) return cudaErrorInvalidValue;
   if (TX + 2 * r > THREADS) return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(NC, r, LP);
-  cudaError_t e = cudaFuncSetAttribute(k_stats4<NC, LP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_stats4<NC, LP, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (y0 >= y1) return cudaSuccess;
   // band height from (W, H) only (see k_stats4): >= ~6 CTAs per SM over the whole image where it allows,
@@ -198,8 +201,16 @@ cudaError_t stats4_launch(const float* G, float* stats, int W, int H, int r, dou
   int BH = 128;
   while (BH > 16 && (long long)strips * ((H + BH - 1) / BH) < 6 * 148) BH /= 2;
   dim3 grid(strips, (y1 + BH - 1) / BH - y0 / BH);
-  k_stats4<NC, LP><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout, wo);
+  k_stats4<NC, LP, RT><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout, wo);
   return cudaGetLastError();
+}
+
+template <int NC, int LP>
+cudaError_t stats4_launch(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos,
+                          float lam0f, int y0, int y1, const float* P, float* wout, WLayout wo, cudaStream_t st) {
+  if (r == 9)   // the paper's / BASELINE's radius
+    return stats4_launch_r<NC, LP, 9>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, P, wout, wo, st);
+  return stats4_launch_r<NC, LP, 0>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, P, wout, wo, st);
 }
 
 template <int NC>
