@@ -94,7 +94,8 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     k_agg6(const __grid_constant__ CUtensorMap tm, const float* __restrict__ G, int W, int H, int L, int label_base,
            float* __restrict__ filtered_out, int do_wta, int first, int last, float* __restrict__ best_cost,
            int32_t* __restrict__ best_label, int32_t* __restrict__ labels_out, float* __restrict__ min_cost_out,
-           int64_t* __restrict__ keys_out, long long* const* __restrict__ peer_keys, int rows_per_owner) {
+           int64_t* __restrict__ keys_out, long long* const* __restrict__ peer_keys, int rows_per_owner,
+           long long* __restrict__ fkeys) {
   using Gm = Geom<NC, R, D>;
   using Ro = Roles<NC, D>;
   constexpr int K = Gm::K, BX = Gm::BX, BY = Gm::BY, PSTRIDE = Gm::PSTRIDE, NV4 = Gm::NV4, KX = Gm::KX;
@@ -131,13 +132,18 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     cuda::ptx::fence_mbarrier_init(cuda::ptx::sem_release, cuda::ptx::scope_cluster);
   }
   __syncthreads();
-  const int S = K * L;
+  // label split (small frames, fewer tiles than ~1.5 waves): CTA z takes labels [la, la + LL) of the chunk and
+  // atomic-MINs its per-pixel minimum keys into fkeys (k_keys_finalize writes the outputs); ties keep the lowest
+  // label either way (the key's low word), so the result equals the unsplit scan
+  const int la = (int)(((long long)L * blockIdx.z) / gridDim.z);
+  const int LL = (int)(((long long)L * (blockIdx.z + 1)) / gridDim.z) - la;
+  const int S = K * LL;
 
   if (wq == THREADS / 32 - 1) {
     // ---- producer: plane k of slice l into buffer k once the owners have released slice l - 1's plane k
     if (ln != 0) return;
     for (int s = 0; s < S; ++s) {
-      const int l = s / K, k = s - l * K, b = s % NB;
+      const int ll = s / K, k = s - ll * K, b = s % NB, l = la + ll;
       if (s >= NB) {
         mbar_wait(&hdone[b], (s / NB - 1) & 1);
         cuda::ptx::fence_proxy_async(cuda::ptx::space_shared);
@@ -203,7 +209,7 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     invN[j] = in ? 1.0f / (float)window_count(gy, gx, H, W, R) : 0.0f;
     best[j] = INFINITY;
     bl[j] = 0;
-    if (do_wta && !first && in) {
+    if (do_wta && !first && !fkeys && in) {
       best[j] = best_cost[p];
       bl[j] = best_label[p];
     }
@@ -228,10 +234,10 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
   }
   float z[KX];
 #pragma unroll 1
-  for (int l = 0; l < L; ++l) {
+  for (int l = la; l < la + LL; ++l) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int sg = l * K + k, b = sg % NB;
+      const int sg = (l - la) * K + k, b = sg % NB;
       const float* lb = buf + b * PSTRIDE;
       mbar_wait(&vdone[b], (sg / NB) & 1);
       float f[4 * NV4];
@@ -276,7 +282,9 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
     const int gx = x0 + seg * KX + s;
     if (gy >= H || gx < 0 || gx >= W) continue;
     const long long p = (long long)gy * W + gx;
-    if (last) {
+    if (fkeys) {
+      if (LL > 0) atomicMin(fkeys + p, (long long)pack_key_signed(best[s], bl[s]));
+    } else if (last) {
       if (labels_out) labels_out[p] = bl[s];
       if (min_cost_out) min_cost_out[p] = best[s];
       if (keys_out) keys_out[p] = pack_key_signed(best[s], bl[s]);
@@ -291,7 +299,7 @@ __global__ void __maxnreg__((Roles<NC, D>::MAXREG))
       best_label[p] = bl[s];
     }
   }
-  if (last && peer_keys) __threadfence_system();
+  if (last && peer_keys && !fkeys) __threadfence_system();
 }
 
 template <int NC, int R, int D>
@@ -302,11 +310,11 @@ cudaError_t agg6_launch(const void* tmap, const AggArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k_agg6<NC, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int XSHIFT = (kWGroupPx - R % kWGroupPx) % kWGroupPx;
-  dim3 grid((a.W + XSHIFT + TX - 1) / TX, (a.H + TY - 1) / TY);
+  dim3 grid((a.W + XSHIFT + TX - 1) / TX, (a.H + TY - 1) / TY, a.fkeys && a.nsplit > 1 ? a.nsplit : 1);
   k_agg6<NC, R, D><<<grid, Ro::THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), a.G, a.W, a.H, a.L,
                                                     a.label_base, a.filtered_out, a.do_wta, a.first, a.last,
                                                     a.best_cost, a.best_label, a.labels_out, a.min_cost_out,
-                                                    a.keys_out, a.peer_keys, a.rows_per_owner);
+                                                    a.keys_out, a.peer_keys, a.rows_per_owner, a.fkeys);
   return cudaGetLastError();
 }
 

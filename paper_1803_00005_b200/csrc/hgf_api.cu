@@ -68,6 +68,7 @@ struct hgf_ctx {
   bool v5coef = false;         // horizontal-first coefficient kernel (interleaved layout, n <= 6, r <= 9): default
   CUtensorMap tm_g5;           // TMA descriptor over the raw guide planes of G for k_coef5 (box 164 x 1 x m)
   bool v5agg = false;          // row-marching aggregation k_agg5 (default after k_coef5, n <= 6, r <= 9)
+  int nsm = 148;                // SMs of the handle's device
   bool v6agg = false;          // warp-specialised aggregation k_agg6 (default on the interleaved layout, n <= 6)
   CUtensorMap tm_w6;           // k_agg6: rank-5 map over wbuf, one-plane box, 64-byte swizzle
   CUtensorMap tm_w5;           // k_agg5: rank-5 map over wbuf, box (16, 4, 6, 1, n + 1), 64-byte swizzle
@@ -474,17 +475,31 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
       return cuda_fail(h, e, "join");
     return HGF_OK;
   }
-  if (h->v5agg && !h->planar_now && do_wta) {
-    // k_agg5 merges every CTA's band minima into the frame's key buffer: start from the MIN identity
-    cudaError_t e = traced(h, HGF_KC_KEYS, h->stream,
-                           [&] { return hgf::launch_fill_i64(h->fkeys, HW, 0x7fffffffffffffffLL, h->stream); });
-    if (e != cudaSuccess) return cuda_fail(h, e, "keys fill");
-  }
   // balanced chunks (e.g. 256 labels with a 147-label capacity -> 2 x 128, not 128 + 128 + ... tails)
   const int nchunks = (L + h->lcap - 1) / h->lcap;
   int step = (L + nchunks - 1) / nchunks;
   step = (step + hgf::kWGroupLabels - 1) / hgf::kWGroupLabels * hgf::kWGroupLabels;
   if (step > h->lcap) step = h->lcap;
+  // small frames on k_agg6 (fewer tiles than ~1.5 waves): split each tile's labels over several CTAs, merged by
+  // 64-bit atomic MIN into the frame's key buffer (HGF_AGG6_SPLIT=0: off)
+  const char* se = std::getenv("HGF_AGG6_SPLIT");
+  const bool split6 = h->v6agg && !h->planar_now && do_wta && !(se && se[0] == '0') &&
+                      hgf::agg6_split(h->W, h->H, h->r, step < L ? step : L, h->nsm) > 1;
+  if (split6 && !h->fkeys) {
+    cudaError_t e = cudaMalloc(&h->fkeys, sizeof(int64_t) * HW);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      h->fkeys = nullptr;
+      return cuda_fail(h, e, "key buffer");
+    }
+  }
+  const bool keyed = (h->v5agg || split6) && !h->planar_now && do_wta;
+  if (keyed) {
+    // k_agg5 / split k_agg6 merge every CTA's minima into the frame's key buffer: start from the MIN identity
+    cudaError_t e = traced(h, HGF_KC_KEYS, h->stream,
+                           [&] { return hgf::launch_fill_i64(h->fkeys, HW, 0x7fffffffffffffffLL, h->stream); });
+    if (e != cudaSuccess) return cuda_fail(h, e, "keys fill");
+  }
   for (int c0 = 0; c0 < L; c0 += step) {
     const int Lc = (L - c0 < step) ? (L - c0) : step;
     const float* chunk = vol ? vol + (long long)c0 * HW : nullptr;
@@ -509,10 +524,14 @@ hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, 
     a.keys_out = keys_out;
     a.peer_keys = h->peer_keys;
     a.rows_per_owner = h->rows_per_owner;
+    if (split6) {
+      a.fkeys = reinterpret_cast<long long*>(h->fkeys);
+      a.nsplit = hgf::agg6_split(h->W, h->H, h->r, Lc, h->nsm);
+    }
     e = launch_agg_chunk(h, a);
     if (e != cudaSuccess) return cuda_fail(h, e, "agg");
   }
-  if (h->v5agg && !h->planar_now && do_wta && (labels_out || min_cost_out || keys_out || h->peer_keys)) {
+  if (keyed && (labels_out || min_cost_out || keys_out || h->peer_keys)) {
     cudaError_t e = traced(h, HGF_KC_KEYS, h->stream, [&] {
       return hgf::launch_keys_finalize(h->fkeys, h->W, h->H, labels_out, min_cost_out, keys_out, h->peer_keys,
                                        h->rows_per_owner, h->stream);
@@ -573,6 +592,7 @@ hgf_status hgf_create_ex(hgf_handle* out, int W, int H, int n_guide, int poly_de
   h->r = radius; h->eps = eps; h->mode = mode;
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   cudaGetDevice(&h->device);
+  cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device);
   const size_t HW = (size_t)W * H;
   const int K = h->n + 1;
   {

@@ -354,6 +354,17 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
       const long long cost = (ctas + 147) / 148 * (bh + 2 * R);
       if (best < 0 || cost < best) { best = cost; BH = bh; }
     }
+    if (most < 148) {
+      // small frames (less than one wave even at 32-row bands, e.g. the paper's 450 x 375 Middlebury size): bands
+      // down to 8 rows, the count minimising waves x (band + warm-up) -- one full wave of short bands beats a
+      // partial wave of long ones
+      for (int nb = nbmin; nb <= H / 8; ++nb) {
+        const int bh = (H + nb - 1) / nb;
+        const long long ctas = (long long)strips * ((H + bh - 1) / bh) * batches;
+        const long long cost = (ctas + 147) / 148 * (bh + 2 * R);
+        if (cost < best) { best = cost; BH = bh; }
+      }
+    }
   }
   const int bh_env = std::getenv("HGF_COEF5_BH") ? std::atoi(std::getenv("HGF_COEF5_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning / test runs only

@@ -25,6 +25,11 @@ struct AggArgs {
   // buffer of the rank owning its row: peer_keys[gy / rows_per_owner][(gy % rows_per_owner) * W + gx]
   long long* const* peer_keys;
   int rows_per_owner;
+  // k_agg6 label split (small frames): nsplit CTAs per tile over disjoint label ranges, each atomic-MINing its
+  // minimum keys (pack_key_signed) into fkeys[H][W]; the caller fills fkeys with the MIN identity before the first
+  // chunk and runs launch_keys_finalize after the last (best_cost / best_label / first / last are not used)
+  int nsplit;
+  long long* fkeys;
 };
 
 // Gp (nullable; used when d == 2): (I_i, I_i^2) pairs, layout [H][m][gp_pitch][2], for k_coef5.
@@ -149,6 +154,14 @@ cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int 
 // label-interleaved layout, n <= 6, r <= 9; tm: rank-5 map over the coefficient buffer with a one-plane box
 // (16, 1, ceil32(64 + 2r) / 16, kAgg6TY + 2r, 1), 64-byte swizzle.  Same AggArgs contract as k_agg3 (a.il == 1).
 constexpr int kAgg6MaxN = 6, kAgg6TY = 48;
+// k_agg6's label split for a frame of W x H: parts per tile so that the grid reaches ~2 waves on nsm SMs (1 = none)
+inline int agg6_split(int W, int H, int r, int L, int nsm) {
+  const long long tiles = (long long)((W + (16 - r % 16) % 16 + 63) / 64) * ((H + kAgg6TY - 1) / kAgg6TY);
+  if (tiles * 2 >= 3LL * nsm) return 1;
+  long long s = (2LL * nsm + tiles - 1) / tiles;
+  const long long smax = L / 4 > 1 ? L / 4 : 1;        // >= 4 labels per part
+  return (int)(s < smax ? s : smax);
+}
 // m, d: guide channels and degree (the owners of m <= 3 hold the raw channels; HGF_AGG6_KX=8 forces the planes).
 cudaError_t launch_agg_v6(int m, int d, int r, const void* tm, const AggArgs& a, cudaStream_t st);
 // keys[H][W] -> labels_out / min_cost_out / keys_out (each nullable) and, when peer_keys != null, a system-scope

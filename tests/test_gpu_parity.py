@@ -701,3 +701,27 @@ def test_agg6_bit_identical_to_agg3(monkeypatch, W, H, L, m, d, r, budget, kx):
         Z = O.hgf_filter(I, V, 0.05, r, d)
         check_z(a["filtered"], Z, float(np.abs(V).max()))
         check_labels(a["labels"], Z, float(np.abs(V).max()))
+
+
+@pytest.mark.parametrize("W,H,L,budget", [(300, 140, 40, None), (450, 375, 60, None), (208, 72, 100, "1")])
+def test_agg6_label_split_bit_identical(monkeypatch, W, H, L, budget):
+    """Small frames (fewer k_agg6 tiles than ~1.5 waves) split each tile's labels over several CTAs merged by 64-bit
+    atomic MIN keys: labels, minimum cost, keys and filtered costs equal the unsplit run bit for bit (ties keep the
+    lowest label through the key's low word), also across coefficient-buffer chunks."""
+    torch = _torch()
+    scene = synth.make_stereo_scene(W, H, L, seed=L)
+    g = torch.from_numpy(scene.left).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    if budget:
+        monkeypatch.setenv("HGF_COEF_BUDGET_MB", budget)
+    out = {}
+    for split in ("1", "0"):
+        monkeypatch.setenv("HGF_AGG6_SPLIT", split)
+        h = _hgf(W, H, 3, 2, 9, 0.05)
+        assert h.kernel_path == "coef5+agg6"
+        o = h.aggregate_wta_ex(g, vol, labels=True, min_cost=True, keys=True, filtered=True)
+        torch.cuda.synchronize()
+        out[split] = {k: v.cpu().numpy() for k, v in o.items()}
+        h.close()
+    for k in ("filtered", "labels", "min_cost", "keys"):
+        assert np.array_equal(out["1"][k], out["0"][k]), k
