@@ -154,13 +154,20 @@ cudaError_t launch_agg_v5(int n, const void* tm_w, const void* tm_g, int W, int 
 // label-interleaved layout, n <= 6, r <= 9; tm: rank-5 map over the coefficient buffer with a one-plane box
 // (16, 1, ceil32(64 + 2r) / 16, kAgg6TY + 2r, 1), 64-byte swizzle.  Same AggArgs contract as k_agg3 (a.il == 1).
 constexpr int kAgg6MaxN = 6, kAgg6TY = 48;
-// k_agg6's label split for a frame of W x H: parts per tile so that the grid reaches ~2 waves on nsm SMs (1 = none)
+// k_agg6's label split for a frame of W x H (1 = none): frames of fewer than ~1.5 waves of tiles take the part count
+// s minimising waves(tiles * s) x (L / s + 2), the 2 standing for a CTA's fixed cost (prologue, pipeline fill and
+// drain) in slice-times; >= 4 labels per part
 inline int agg6_split(int W, int H, int r, int L, int nsm) {
   const long long tiles = (long long)((W + (16 - r % 16) % 16 + 63) / 64) * ((H + kAgg6TY - 1) / kAgg6TY);
   if (tiles * 2 >= 3LL * nsm) return 1;
-  long long s = (2LL * nsm + tiles - 1) / tiles;
-  const long long smax = L / 4 > 1 ? L / 4 : 1;        // >= 4 labels per part
-  return (int)(s < smax ? s : smax);
+  const int smax = L / 4 > 1 ? L / 4 : 1;
+  int best_s = 1;
+  double best = 1e300;
+  for (int s = 1; s <= smax; ++s) {
+    const double cost = (double)((tiles * s + nsm - 1) / nsm) * ((double)L / s + 2.0);
+    if (cost < best) { best = cost; best_s = s; }
+  }
+  return best_s;
 }
 // m, d: guide channels and degree (the owners of m <= 3 hold the raw channels; HGF_AGG6_KX=8 forces the planes).
 cudaError_t launch_agg_v6(int m, int d, int r, const void* tm, const AggArgs& a, cudaStream_t st);
