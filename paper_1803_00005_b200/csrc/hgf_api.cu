@@ -69,6 +69,7 @@ struct hgf_ctx {
   CUtensorMap tm_g5;           // TMA descriptor over the raw guide planes of G for k_coef5 (box 164 x 1 x m)
   bool v5agg = false;          // row-marching aggregation k_agg5 (default after k_coef5, n <= 6, r <= 9)
   int nsm = 148;                // SMs of the handle's device
+  int lmodel = 0;               // labels of the current call (k_coef5's band height is chosen for it)
   bool v6agg = false;          // warp-specialised aggregation k_agg6 (default on the interleaved layout, n <= 6)
   CUtensorMap tm_w6;           // k_agg6: rank-5 map over wbuf, one-plane box, 64-byte swizzle
   CUtensorMap tm_w5;           // k_agg5: rank-5 map over wbuf, box (16, 4, 6, 1, n + 1), 64-byte swizzle
@@ -310,6 +311,7 @@ cudaError_t launch_coef_chunk(hgf_ctx* h, const float* guide, const float* vol_c
                          hgf::kCoef5LB))
         return cudaErrorInvalidValue;
       return hgf::launch_coef_v5(h->m, h->d, &tm_vol, &h->tm_g5, h->stats, wdst, h->wlay, h->W, h->H, h->r, Lc,
+                                 h->lmodel,
                                  h->stream);
     }
     if (h->v3coef) {
@@ -412,6 +414,7 @@ template <class BuildChunk>
 hgf_status slices_impl(hgf_ctx* h, const float* guide, const float* vol, int L, int label_offset, float* filtered_out,
                        int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out, BuildChunk build_chunk) {
   const long long HW = (long long)h->W * h->H;
+  h->lmodel = L;
   // opt-in (HGF_PIPELINE=1): measured slower at C4 (36.3 vs 35.2 ms: the overlapped kernels slow each other down
   // -- coef 14.8 -> 20.5 ms, agg 19.2 -> 27.3 ms of device time -- on top of 4 chunks' tails instead of 2)
   const bool pipe_env = std::getenv("HGF_PIPELINE") && std::getenv("HGF_PIPELINE")[0] == '1';
@@ -1211,6 +1214,7 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
   if ((s = frame_stats(h, h->st_guide, 0, h->H)) != HGF_OK) return s;
   const long long lcap = h->st_chunk;
   const int nchunks = (int)((L + lcap - 1) / lcap);
+  h->lmodel = L;
   if (h->v5agg) {
     e = traced(h, HGF_KC_KEYS, h->stream,
                [&] { return hgf::launch_fill_i64(h->fkeys, (long long)HW, 0x7fffffffffffffffLL, h->stream); });

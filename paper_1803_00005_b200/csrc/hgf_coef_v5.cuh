@@ -329,14 +329,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
 
 template <int M, int D, int R>
 cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, float* wbuf, WLayout wo, int W, int H,
-                    int L, cudaStream_t st) {
+                    int L, int Lmodel, cudaStream_t st) {
   using Gm = Geom<M * D>;
   cudaError_t e = cudaFuncSetAttribute(k_coef5<M, D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
   if (e != cudaSuccess) return e;
   // band height: one CTA per SM; a band of BH rows costs BH + 2R steps (the vertical warm-up), so pick the
   // band count minimising waves x (BH + 2R), waves = ceil(CTAs / 148), among band counts giving >= 8 waves
   // (or, for small images, the most CTAs) -- the same wave model as k_coef3.
-  const int strips = (W + TX - 1) / TX, batches = (L + LB - 1) / LB;
+  // the band height depends on (W, H, R, Lmodel) only (see launch_coef_v5); the grid uses this chunk's batches
+  const int strips = (W + TX - 1) / TX, batches = ((Lmodel > L ? Lmodel : L) + LB - 1) / LB;
+  const int chunk_batches = (L + LB - 1) / LB;
   constexpr int kMaxBand = 320;
   int BH = H < kMaxBand ? H : kMaxBand;
   {
@@ -368,7 +370,7 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
   }
   const int bh_env = std::getenv("HGF_COEF5_BH") ? std::atoi(std::getenv("HGF_COEF5_BH")) : 0;
   if (bh_env >= 8) BH = bh_env;                    // tuning / test runs only
-  dim3 grid(batches, strips, (H + BH - 1) / BH);
+  dim3 grid(chunk_batches, strips, (H + BH - 1) / BH);
   k_coef5<M, D, R><<<grid, NW * 32, Gm::SMEM, st>>>(*reinterpret_cast<const CUtensorMap*>(tm_vol),
                                                     *reinterpret_cast<const CUtensorMap*>(tm_i), stats, wbuf, wo, W, H,
                                                     L, BH);
@@ -377,17 +379,17 @@ cudaError_t coef5_r(const void* tm_vol, const void* tm_i, const float* stats, fl
 
 template <int M, int D>
 cudaError_t coef5_impl(const void* tm_vol, const void* tm_i, const float* stats, float* wbuf, WLayout wo, int W,
-                       int H, int r, int L, cudaStream_t st) {
+                       int H, int r, int L, int Lmodel, cudaStream_t st) {
   switch (r) {
-    case 1: return coef5_r<M, D, 1>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 2: return coef5_r<M, D, 2>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 3: return coef5_r<M, D, 3>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 4: return coef5_r<M, D, 4>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 5: return coef5_r<M, D, 5>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 6: return coef5_r<M, D, 6>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 7: return coef5_r<M, D, 7>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 8: return coef5_r<M, D, 8>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
-    case 9: return coef5_r<M, D, 9>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, st);
+    case 1: return coef5_r<M, D, 1>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 2: return coef5_r<M, D, 2>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 3: return coef5_r<M, D, 3>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 4: return coef5_r<M, D, 4>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 5: return coef5_r<M, D, 5>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 6: return coef5_r<M, D, 6>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 7: return coef5_r<M, D, 7>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 8: return coef5_r<M, D, 8>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
+    case 9: return coef5_r<M, D, 9>(tm_vol, tm_i, stats, wbuf, wo, W, H, L, Lmodel, st);
     default: return cudaErrorInvalidValue;
   }
 }

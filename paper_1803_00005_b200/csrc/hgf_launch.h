@@ -176,8 +176,10 @@ cudaError_t launch_agg_v6(int m, int d, int r, const void* tm, const AggArgs& a,
 cudaError_t launch_keys_finalize(const int64_t* keys, int W, int H, int32_t* labels_out, float* min_cost_out,
                                  int64_t* keys_out, long long* const* peer_keys, int rows_per_owner, cudaStream_t st);
 bool coef5_ok(int m, int d, int r);
+// Lmodel: the label count the band height is chosen for (the whole call's, so every chunk of a call -- and a call
+// whatever its chunking -- marches the same bands and gives the same bits); L: this chunk's labels.
 cudaError_t launch_coef_v5(int m, int d, const void* tm_vol, const void* tm_i, const float* stats, float* wbuf,
-                           WLayout wo, int W, int H, int r, int L, cudaStream_t st);
+                           WLayout wo, int W, int H, int r, int L, int Lmodel, cudaStream_t st);
 }  // namespace hgf
 
 namespace hgf {
