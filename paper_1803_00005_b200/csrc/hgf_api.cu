@@ -1193,7 +1193,10 @@ hgf_status hgf_aggregate_wta_host(hgf_handle h, const float* guide_host, const f
   const size_t HW = (size_t)h->W * h->H;
   cudaError_t e;
   if (!h->st_guide) {
-    h->st_chunk = h->lcap;
+    // 32-label staging chunks (one label batch of the slice kernels): the H2D copy of chunk c + 1 overlaps the
+    // aggregation of chunk c (with whole-call chunks the copy and the compute ran back to back); the band heights
+    // are chosen for the whole call (lmodel), so the result is the device path's bit for bit
+    h->st_chunk = h->lcap < hgf::kWGroupLabels ? h->lcap : hgf::kWGroupLabels;
     if ((e = cudaMalloc(&h->st_guide, sizeof(float) * h->m * HW)) != cudaSuccess ||
         (e = cudaMalloc(&h->st_vol[0], sizeof(float) * HW * h->st_chunk)) != cudaSuccess ||
         (e = cudaMalloc(&h->st_vol[1], sizeof(float) * HW * h->st_chunk)) != cudaSuccess ||

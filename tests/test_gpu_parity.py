@@ -229,11 +229,14 @@ def test_shard_merge_equals_unsharded():
     assert np.array_equal(cost.cpu().numpy(), full["min_cost"])
 
 
-def test_host_entry_point_matches_device():
+@pytest.mark.parametrize("W,H,L", [(40, 30, 7), (160, 90, 100)])
+def test_host_entry_point_matches_device(W, H, L):
+    """hgf_aggregate_wta_host (pageable host buffers, 32-label staging chunks double-buffered against the compute)
+    gives the device path's labels bit for bit, also over several chunks."""
     torch = _torch()
-    I, V = synth.iid_volume(40, 30, 7, 3, seed=9)
+    I, V = synth.iid_volume(W, H, L, 3, seed=9)
     dev = _run(I, V, 2, 3, 0.05)
-    h = _hgf(40, 30, 3, 2, 3, 0.05)
+    h = _hgf(W, H, 3, 2, 3, 0.05)
     lab = h.aggregate_wta_host(torch.from_numpy(I), torch.from_numpy(V))
     assert np.array_equal(lab.numpy(), dev["labels"])
 
