@@ -18,6 +18,7 @@
 // Pitches are odd in doubles so that the H phase's pair-strided accesses spread over the banks.
 // fp32 x fp32 products are exact in float64; a running sum accumulates at most BH + 2r + 1 row updates.
 #pragma once
+#include <cstdlib>
 #include "hgf_common.cuh"
 #include "hgf_launch.h"
 #include "hgf_stats_finish.cuh"
@@ -195,11 +196,16 @@ cudaError_t stats4_launch_r(const float* G, float* stats, int W, int H, int r, d
   cudaError_t e = cudaFuncSetAttribute(k_stats4<NC, LP, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (y0 >= y1) return cudaSuccess;
-  // band height from (W, H) only (see k_stats4): >= ~6 CTAs per SM over the whole image where it allows,
-  // bands long enough to amortise the 2r+1-row warm-up
+  // band height from (W, H) only (see k_stats4: row-sharded statistics stay bit-identical): >= ~6 CTAs per SM over
+  // the whole image where it allows, bands of at most 64 rows (measured at C4: 64 -> 0.89 ms, 128 -> 0.95 ms; a
+  // waves x (band + warm-up) model picked badly for the fused single-slice pass at r = 4, HGF_STATS4_BH sweeps)
   const int strips = (W + TX - 1) / TX;
-  int BH = 128;
+  int BH = 64;
   while (BH > 16 && (long long)strips * ((H + BH - 1) / BH) < 6 * 148) BH /= 2;
+  {
+    const char* e = std::getenv("HGF_STATS4_BH");     // tuning runs only
+    if (e && std::atoi(e) >= 8) BH = std::atoi(e);
+  }
   dim3 grid(strips, (y1 + BH - 1) / BH - y0 / BH);
   k_stats4<NC, LP, RT><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout, wo);
   return cudaGetLastError();
