@@ -159,7 +159,8 @@ constexpr int kAgg6MaxN = 6, kAgg6TY = 48;
 // drain) in slice-times; >= 4 labels per part
 inline int agg6_split(int W, int H, int r, int L, int nsm) {
   const long long tiles = (long long)((W + (16 - r % 16) % 16 + 63) / 64) * ((H + kAgg6TY - 1) / kAgg6TY);
-  if (tiles * 2 >= 3LL * nsm) return 1;
+  // (fewer than 32 labels: the key fill + finalize launches cost more than the split saves)
+  if (tiles * 2 >= 3LL * nsm || L < 32) return 1;
   const int smax = L / 4 > 1 ? L / 4 : 1;
   int best_s = 1;
   double best = 1e300;
