@@ -149,16 +149,19 @@ __global__ void __launch_bounds__(THREADS) k_stats4(const float* __restrict__ G,
     }
     if (yb + RB <= Z0) continue;                 // rows before the requested range: V only (same thread)
     __syncthreads();
-    // ---- H phase: sliding 2r+1-column window sums per (rb, segment, pair)
-    for (int item = tid; item < ((HGF_ST4_EXP & 2) ? 0 : RB * NSEG * NPAIR); item += THREADS) {
-      const int q = item % NPAIR, sg = (item / NPAIR) % NSEG, rb = item / (NPAIR * NSEG);
-      const double* v = vs + (rb * NPAIR + q) * VXP + sg * HSEG;
-      double* o = hs + (rb * NPAIR + q) * TXP + sg * HSEG;
+    // ---- H phase: sliding 2r+1-column window sums per (rb, segment, pair); 32-pixel segments when all the items
+    // then fit one pass of the CTA (fewer window re-reads: 2.5 instead of 3 loads per output; C4 -6 %), else 16
+    constexpr int HS = RB * (TX / 32) * NPAIR <= THREADS ? 32 : HSEG;
+    constexpr int NS = TX / HS;
+    for (int item = tid; item < ((HGF_ST4_EXP & 2) ? 0 : RB * NS * NPAIR); item += THREADS) {
+      const int q = item % NPAIR, sg = (item / NPAIR) % NS, rb = item / (NPAIR * NS);
+      const double* v = vs + (rb * NPAIR + q) * VXP + sg * HS;
+      double* o = hs + (rb * NPAIR + q) * TXP + sg * HS;
       double a = 0.0;
       for (int j = 0; j <= 2 * r; ++j) a += v[j];
       o[0] = a;
 #pragma unroll
-      for (int i = 1; i < HSEG; ++i) {
+      for (int i = 1; i < HS; ++i) {
         a += v[i + 2 * r] - v[i - 1];
         o[i] = a;
       }
