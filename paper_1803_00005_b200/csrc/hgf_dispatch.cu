@@ -101,7 +101,7 @@ cudaError_t launch_filter1(int n, const float* G, const float* P, float* wout, W
   if (n > kStats4MaxN || 64 + 2 * r > 128 || stats4_smem(n, r, 1) > 200 * 1024) return cudaErrorInvalidValue;
   switch (n) {
 #define F1(N) \
-  case N: return st4::filter1_impl<N>(G, P, wout, wo, W, H, r, lam, mode, lam0f, st);
+  case N: return st5::filter1_sel<N>(G, P, wout, wo, W, H, r, lam, mode, lam0f, st);
     F1(1) F1(2) F1(3) F1(4) F1(5) F1(6) F1(7) F1(8) F1(9)
 #undef F1
     default: return cudaErrorInvalidValue;
@@ -119,15 +119,15 @@ cudaError_t launch_stats(int n, const float* G, float* stats, int W, int H, int 
   const bool force2 = std::getenv("HGF_STATS2") != nullptr && std::getenv("HGF_STATS2")[0] == '1';
   if (!force2 && n <= kStats4MaxN && 64 + 2 * r <= 128 && stats4_smem(n, r) <= 200 * 1024) {
     switch (n) {
-      case 1: return st4::stats4_impl<1>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 2: return st4::stats4_impl<2>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 3: return st4::stats4_impl<3>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 4: return st4::stats4_impl<4>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 5: return st4::stats4_impl<5>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 6: return st4::stats4_impl<6>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 7: return st4::stats4_impl<7>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 8: return st4::stats4_impl<8>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
-      case 9: return st4::stats4_impl<9>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 1: return st5::stats_sel<1>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 2: return st5::stats_sel<2>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 3: return st5::stats_sel<3>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 4: return st5::stats_sel<4>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 5: return st5::stats_sel<5>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 6: return st5::stats_sel<6>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 7: return st5::stats_sel<7>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 8: return st5::stats_sel<8>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
+      case 9: return st5::stats_sel<9>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, st);
       default: break;
     }
   }

@@ -81,4 +81,13 @@ template cudaError_t filter1_impl<HGF_N>(const float*, const float*, float*, WLa
                                          float, cudaStream_t);
 }  // namespace st4
 }  // namespace hgf
+#include "hgf_stats_v5.cuh"
+namespace hgf {
+namespace st5 {
+template cudaError_t stats_sel<HGF_N>(const float*, float*, int, int, int, double, int, int, float, int, int,
+                                      cudaStream_t);
+template cudaError_t filter1_sel<HGF_N>(const float*, const float*, float*, WLayout, int, int, int, double, int,
+                                        float, cudaStream_t);
+}  // namespace st5
+}  // namespace hgf
 #endif

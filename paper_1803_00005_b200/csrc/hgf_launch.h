@@ -202,4 +202,12 @@ template <int NC>
 cudaError_t filter1_impl(const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r, double lam,
                          int mode, float lam0f, cudaStream_t st);
 }  // namespace st4
+namespace st5 {
+template <int NC>
+cudaError_t stats_sel(const float* G, float* stats, int W, int H, int r, double lam, int mode, int aos, float lam0f,
+                      int y0, int y1, cudaStream_t st);
+template <int NC>
+cudaError_t filter1_sel(const float* G, const float* P, float* wout, WLayout wo, int W, int H, int r, double lam,
+                        int mode, float lam0f, cudaStream_t st);
+}  // namespace st5
 }  // namespace hgf

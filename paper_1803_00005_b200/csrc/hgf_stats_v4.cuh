@@ -45,6 +45,19 @@ __host__ __device__ inline size_t smem_bytes(int NC, int r, int lp = 0) {
   return (size_t)RB * nsums(NC, lp) * (vx_pitch(r) + TXP) * sizeof(double);
 }
 
+// Band height from (W, H) only (row-sharded statistics stay bit-identical, also between k_stats4 and k_stats5):
+// >= ~6 CTAs per SM over the whole image where it allows, bands of at most 64 rows (measured at C4: 64 -> 0.89 ms,
+// 128 -> 0.95 ms; a waves x (band + warm-up) model picked badly for the fused single-slice pass at r = 4;
+// HGF_STATS4_BH sweeps).
+inline int band_height(int W, int H) {
+  const int strips = (W + TX - 1) / TX;
+  int BH = 64;
+  while (BH > 16 && (long long)strips * ((H + BH - 1) / BH) < 6 * 148) BH /= 2;
+  const char* e = std::getenv("HGF_STATS4_BH");     // tuning runs only
+  if (e && std::atoi(e) >= 8) BH = std::atoi(e);
+  return BH;
+}
+
 // Rows [yb0, yb1).  CTA (bx, by) owns columns [bx*TX, +TX) and the absolute band of rows
 // [(yb0/BH + by)*BH, +BH), BH a function of (W, H) only: every row's running sums have the same history
 // whichever row range is requested, so row-sharded statistics are bit-identical to the full pass.
@@ -199,16 +212,8 @@ cudaError_t stats4_launch_r(const float* G, float* stats, int W, int H, int r, d
   cudaError_t e = cudaFuncSetAttribute(k_stats4<NC, LP, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (y0 >= y1) return cudaSuccess;
-  // band height from (W, H) only (see k_stats4: row-sharded statistics stay bit-identical): >= ~6 CTAs per SM over
-  // the whole image where it allows, bands of at most 64 rows (measured at C4: 64 -> 0.89 ms, 128 -> 0.95 ms; a
-  // waves x (band + warm-up) model picked badly for the fused single-slice pass at r = 4, HGF_STATS4_BH sweeps)
   const int strips = (W + TX - 1) / TX;
-  int BH = 64;
-  while (BH > 16 && (long long)strips * ((H + BH - 1) / BH) < 6 * 148) BH /= 2;
-  {
-    const char* e = std::getenv("HGF_STATS4_BH");     // tuning runs only
-    if (e && std::atoi(e) >= 8) BH = std::atoi(e);
-  }
+  const int BH = band_height(W, H);
   dim3 grid(strips, (y1 + BH - 1) / BH - y0 / BH);
   k_stats4<NC, LP, RT><<<grid, THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout, wo);
   return cudaGetLastError();

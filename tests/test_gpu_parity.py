@@ -728,3 +728,25 @@ def test_agg6_label_split_bit_identical(monkeypatch, W, H, L, budget):
         h.close()
     for k in ("filtered", "labels", "min_cost", "keys"):
         assert np.array_equal(out["1"][k], out["0"][k]), k
+
+
+@pytest.mark.parametrize("W,H,L,m,d,r", [(300, 140, 40, 3, 2, 9), (133, 71, 9, 2, 3, 4), (90, 200, 5, 1, 1, 16)])
+def test_stats5_bit_identical_to_stats4(monkeypatch, W, H, L, m, d, r):
+    """k_stats5 (warp-specialised statistics pass: vertical / horizontal / recursion warps pipelined through
+    mbarriers) performs k_stats4's arithmetic in k_stats4's order: the aggregated results are bit-identical
+    (HGF_STATS5=0 runs k_stats4)."""
+    torch = _torch()
+    scene = synth.make_stereo_scene(W, H, L, seed=W)
+    I = np.ascontiguousarray(synth.smooth_guides(W, H, m, seed=W)) if m != 3 else scene.left
+    g = torch.from_numpy(I).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    out = {}
+    for s5 in ("1", "0"):
+        monkeypatch.setenv("HGF_STATS5", s5)         # 1: k_stats5 also for the statistics pass
+        h = _hgf(W, H, m, d, r, 0.05)
+        o = h.aggregate_wta_ex(g, vol, labels=True, filtered=True)
+        torch.cuda.synchronize()
+        out[s5] = {k: v.cpu().numpy() for k, v in o.items()}
+        h.close()
+    for k in ("filtered", "labels"):
+        assert np.array_equal(out["1"][k], out["0"][k]), k
