@@ -69,15 +69,27 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
   uint64_t* hfull = vfree + NBV;                         // H wrote slot (NHW warps)
   uint64_t* hfree = hfull + NBH;                         // R read slot (NRW warps)
   const int tid = threadIdx.x, wq = tid >> 5, ln = tid & 31;
-  const int x0 = blockIdx.x * TX;
-  const int Y0 = (yb0 / BH + (int)blockIdx.y) * BH, Y1 = min(H, Y0 + BH);
-  const int Z0 = max(Y0, yb0), Z1 = min(Y1, yb1);       // rows written
   const long long HW = (long long)H * W;
-  // iterations yb = Y0 + it * RB while yb < Z1; those with yb + RB <= Z0 (rows before the requested range) are
-  // vertical-only; the others, j = it - it0, go through the slots
-  const int nit = Z1 > Y0 ? (Z1 - Y0 + RB - 1) / RB : 0;
-  const int it0 = Z0 > Y0 ? (Z0 - Y0) / RB : 0;
-  const int nj = nit - it0;
+  // persistent CTAs: work item = (strip, band), strips fastest, items blockIdx.x, + gridDim.x, ...; every role walks
+  // the same items, and the slot counter jg runs on across items, so a CTA's vertical warps start the next band's
+  // warm-up while its horizontal / recursion warps finish the last one
+  const int strips = (W + TX - 1) / TX;
+  const int band0 = yb0 / BH, nbands = (yb1 + BH - 1) / BH - band0;
+  const int nitems = strips * nbands;
+  struct Item { int x0, Y0, Z0, Z1, nit, it0; };
+  auto item_of = [&](int it_) {
+    Item I;
+    I.x0 = (it_ % strips) * TX;
+    I.Y0 = (band0 + it_ / strips) * BH;
+    const int Y1 = min(H, I.Y0 + BH);
+    I.Z0 = max(I.Y0, yb0);
+    I.Z1 = min(Y1, yb1);                                 // rows written
+    // iterations yb = Y0 + it * RB while yb < Z1; those with yb + RB <= Z0 (rows before the requested range) are
+    // vertical-only; the others go through the slots
+    I.nit = I.Z1 > I.Y0 ? (I.Z1 - I.Y0 + RB - 1) / RB : 0;
+    I.it0 = I.Z0 > I.Y0 ? (I.Z0 - I.Y0) / RB : 0;
+    return I;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < NBV; ++s) {
@@ -97,95 +109,102 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
     const int c = tid;
     const int CX = TX + 2 * r;
     const bool vcol = c < CX;
-    const int vx = x0 - r + c;
-    const bool xin = vcol && vx >= 0 && vx < W;
-    auto load_row = [&](int yy, float (&v)[K + LP]) {
-      const bool in = xin && yy >= 0 && yy < H;
-      v[0] = in ? 1.0f : 0.0f;
-      const float* src = G + (long long)yy * W + vx;
+    int jg = 0;
+    for (int itm = blockIdx.x; itm < nitems; itm += gridDim.x) {
+      const Item I = item_of(itm);
+      const int Y0 = I.Y0, nit = I.nit, it0 = I.it0;
+      const int vx = I.x0 - r + c;
+      const bool xin = vcol && vx >= 0 && vx < W;
+      auto load_row = [&](int yy, float (&v)[K + LP]) {
+        const bool in = xin && yy >= 0 && yy < H;
+        v[0] = in ? 1.0f : 0.0f;
+        const float* src = G + (long long)yy * W + vx;
 #pragma unroll
-      for (int k = 1; k < K; ++k) v[k] = in ? __ldg(src + (k - 1) * HW) : 0.0f;
-      if (LP) v[K] = in ? __ldg(P + (long long)yy * W + vx) : 0.0f;
-    };
-    double acc[NPAIR];
+        for (int k = 1; k < K; ++k) v[k] = in ? __ldg(src + (k - 1) * HW) : 0.0f;
+        if (LP) v[K] = in ? __ldg(P + (long long)yy * W + vx) : 0.0f;
+      };
+      double acc[NPAIR];
 #pragma unroll
-    for (int q = 0; q < NPAIR; ++q) acc[q] = 0.0;
-    // warm-up: the window of output row Y0 - 1 (rows Y0 - 1 - r .. Y0 - 1 + r)
-    if (vcol) {
-      for (int yy = Y0 - 1 - r; yy <= Y0 - 1 + r; ++yy) {
-        float e[K + LP];
-        load_row(yy, e);
-        int q = 0;
-#pragma unroll
-        for (int a = 0; a < K; ++a)
-#pragma unroll
-          for (int b = a; b < K; ++b) {
-            if (a == 0 && b == 0) continue;
-            acc[q] = fma((double)e[a], (double)e[b], acc[q]);
-            ++q;
-          }
-        if constexpr (LP == 1) {
-#pragma unroll
-          for (int a = 0; a < K; ++a) acc[NG + a] = fma((double)e[a], (double)e[K], acc[NG + a]);
-        }
-      }
-    }
-    float en[RB][K + LP], lnx[RB][K + LP];
-    if (vcol && nit > 0) {
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        load_row(Y0 + rb + r, en[rb]);
-        load_row(Y0 + rb - r - 1, lnx[rb]);
-      }
-    }
-    for (int it = 0; it < nit; ++it) {
-      const int yb = Y0 + it * RB, j = it - it0;
-      float e[RB][K + LP], l[RB][K + LP];
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb)
-#pragma unroll
-        for (int a = 0; a < K + LP; ++a) {
-          e[rb][a] = en[rb][a];
-          l[rb][a] = lnx[rb][a];
-        }
-      if (vcol && it + 1 < nit) {
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
-          load_row(yb + RB + rb + r, en[rb]);
-          load_row(yb + RB + rb - r - 1, lnx[rb]);
-        }
-      }
-      const int sv = j >= 0 ? j % NBV : 0;
-      double* dstb = vs + (size_t)sv * RB * NPAIR * VXP;
-      if (j >= NBV) bwait(&vfree[sv], (j / NBV - 1) & 1);
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        if (vcol) {
+      for (int q = 0; q < NPAIR; ++q) acc[q] = 0.0;
+      // warm-up: the window of output row Y0 - 1 (rows Y0 - 1 - r .. Y0 - 1 + r)
+      if (vcol) {
+        for (int yy = Y0 - 1 - r; yy <= Y0 - 1 + r; ++yy) {
+          float e[K + LP];
+          load_row(yy, e);
           int q = 0;
 #pragma unroll
           for (int a = 0; a < K; ++a)
 #pragma unroll
             for (int b = a; b < K; ++b) {
               if (a == 0 && b == 0) continue;
-              acc[q] = fma((double)e[rb][a], (double)e[rb][b], fma(-(double)l[rb][a], (double)l[rb][b], acc[q]));
+              acc[q] = fma((double)e[a], (double)e[b], acc[q]);
               ++q;
             }
           if constexpr (LP == 1) {
 #pragma unroll
-            for (int a = 0; a < K; ++a)
-              acc[NG + a] =
-                  fma((double)e[rb][a], (double)e[rb][K], fma(-(double)l[rb][a], (double)l[rb][K], acc[NG + a]));
-          }
-          if (j >= 0) {
-            double* dst = dstb + rb * NPAIR * VXP + c;
-#pragma unroll
-            for (int q2 = 0; q2 < NPAIR; ++q2) dst[q2 * VXP] = acc[q2];
+            for (int a = 0; a < K; ++a) acc[NG + a] = fma((double)e[a], (double)e[K], acc[NG + a]);
           }
         }
       }
-      if (j >= 0) {
-        __syncwarp();
-        if (ln == 0) barrive(&vfull[sv]);
+      float en[RB][K + LP], lnx[RB][K + LP];
+      if (vcol && nit > 0) {
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          load_row(Y0 + rb + r, en[rb]);
+          load_row(Y0 + rb - r - 1, lnx[rb]);
+        }
+      }
+      for (int it = 0; it < nit; ++it) {
+        const int yb = Y0 + it * RB;
+        const bool slot = it >= it0;
+        float e[RB][K + LP], l[RB][K + LP];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int a = 0; a < K + LP; ++a) {
+            e[rb][a] = en[rb][a];
+            l[rb][a] = lnx[rb][a];
+          }
+        if (vcol && it + 1 < nit) {
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            load_row(yb + RB + rb + r, en[rb]);
+            load_row(yb + RB + rb - r - 1, lnx[rb]);
+          }
+        }
+        const int sv = jg % NBV;
+        double* dstb = vs + (size_t)sv * RB * NPAIR * VXP;
+        if (slot && jg >= NBV) bwait(&vfree[sv], (jg / NBV - 1) & 1);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          if (vcol) {
+            int q = 0;
+#pragma unroll
+            for (int a = 0; a < K; ++a)
+#pragma unroll
+              for (int b = a; b < K; ++b) {
+                if (a == 0 && b == 0) continue;
+                acc[q] = fma((double)e[rb][a], (double)e[rb][b], fma(-(double)l[rb][a], (double)l[rb][b], acc[q]));
+                ++q;
+              }
+            if constexpr (LP == 1) {
+#pragma unroll
+              for (int a = 0; a < K; ++a)
+                acc[NG + a] =
+                    fma((double)e[rb][a], (double)e[rb][K], fma(-(double)l[rb][a], (double)l[rb][K], acc[NG + a]));
+            }
+            if (slot) {
+              double* dst = dstb + rb * NPAIR * VXP + c;
+#pragma unroll
+              for (int q2 = 0; q2 < NPAIR; ++q2) dst[q2 * VXP] = acc[q2];
+            }
+          }
+        }
+        if (slot) {
+          __syncwarp();
+          if (ln == 0) barrive(&vfull[sv]);
+          ++jg;
+        }
       }
     }
     return;
@@ -196,7 +215,10 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
     const int t = tid - 32 * NVW;
     const bool act = t < C::ITEMS;
     const int q = t % NPAIR, sg = (t / NPAIR) % (TX / HS), rb = t / (NPAIR * (TX / HS));
-    for (int j = 0; j < nj; ++j) {
+    int j = 0;
+    for (int itm = blockIdx.x; itm < nitems; itm += gridDim.x) {
+     const Item I = item_of(itm);
+     for (int jj0 = I.it0; jj0 < I.nit; ++jj0, ++j) {
       const int sv = j % NBV, sh = j % NBH;
       bwait(&vfull[sv], (j / NBV) & 1);
       if (j >= NBH) bwait(&hfree[sh], (j / NBH - 1) & 1);
@@ -217,6 +239,7 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
         barrive(&vfree[sv]);
         barrive(&hfull[sh]);
       }
+     }
     }
     return;
   }
@@ -224,7 +247,10 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
   // ---- R warps: pixel (rb, x) of each iteration
   const int p = tid - 32 * (NVW + NHW);
   const int rb = p / TX, x = p % TX;
-  for (int j = 0; j < nj; ++j) {
+  int j = 0;
+  for (int itm = blockIdx.x; itm < nitems; itm += gridDim.x) {
+   const Item I = item_of(itm);
+   for (int it = I.it0; it < I.nit; ++it, ++j) {
     const int sh = j % NBH;
     bwait(&hfull[sh], (j / NBH) & 1);
     double g[NPAIR];
@@ -233,8 +259,8 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
     for (int q = 0; q < NPAIR; ++q) g[q] = src[q * TXP];
     __syncwarp();
     if (ln == 0) barrive(&hfree[sh]);
-    const int gy = Y0 + (it0 + j) * RB + rb, gx = x0 + x;
-    if (gy >= Z0 && gy < Z1 && gx < W) {
+    const int gy = I.Y0 + it * RB + rb, gx = I.x0 + x;
+    if (gy >= I.Z0 && gy < I.Z1 && gx < W) {
       const double N = (double)window_count(gy, gx, H, W, r);
       if constexpr (LP == 1) {
         float* wl = wout + wo.origin + (long long)gy * wo.pitch + gx;
@@ -244,6 +270,7 @@ __global__ void __launch_bounds__(Cfg<NC, LP>::THREADS, 1)
         stats_finish<NC>(g, N, lam, mode, aos, lam0f, stats, (long long)gy * W + gx, HW);
       }
     }
+   }
   }
 }
 
@@ -271,7 +298,14 @@ cudaError_t stats5_launch_r(const float* G, float* stats, int W, int H, int r, d
       if (best < 0 || cost < best) { best = cost; BH = bh; }
     }
   }
-  dim3 grid((W + TX - 1) / TX, (y1 + BH - 1) / BH - y0 / BH);
+  const long long items = (long long)((W + TX - 1) / TX) * ((y1 + BH - 1) / BH - y0 / BH);
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  dim3 grid((unsigned)(items < nsm ? items : nsm));     // persistent: one CTA per SM walking the work items
   k_stats5<NC, LP, RT><<<grid, C::THREADS, smem, st>>>(G, stats, W, H, r, lam, mode, aos, lam0f, y0, y1, BH, P, wout,
                                                       wo);
   return cudaGetLastError();
