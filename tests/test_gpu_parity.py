@@ -479,6 +479,27 @@ def test_peer_merge_equals_allreduce_merge():
     h.close()
 
 
+def test_peer_merge_with_label_split():
+    """The fused merge on a small frame with >= 32 labels, where k_agg6 splits each tile's labels over several CTAs
+    (k_keys_finalize then does the system-scope MIN into the owners): the owner rows equal the one-call keys."""
+    torch = _torch()
+    from paper_1803_00005_b200 import PeerKeys
+    W, H, L = 180, 77, 80
+    scene = synth.make_stereo_scene(W, H, L, seed=92)
+    gi = torch.from_numpy(scene.left).cuda()
+    vol = synth.stereo_cost_volume_torch(scene, L, "cuda")
+    h = _hgf(W, H, 3, 2, 9, 0.05, "hgf")
+    ref = h.aggregate_wta_ex(gi, vol, labels=True, keys=True)
+    pk = PeerKeys(h)
+    pk.reset()
+    h.prepare_rows(gi, 0, H)
+    h.aggregate_wta_peer(vol, pk.ptrs, 1, pk.rows)
+    torch.cuda.synchronize()
+    assert torch.equal(pk.keys, ref["keys"])
+    pk.close()
+    h.close()
+
+
 def test_peer_merge_double_buffered_steps():
     """PeerMerge (the bench's N > 1 step): alternating owner buffers over several steps whose volumes differ,
     each step's labels equal to the one-call path's (a stale buffer would leak the previous step's minima)."""
