@@ -54,6 +54,12 @@ CASES = [
     ("r32-small-image", 20, 17, 3, 2, 3, 32, 0.05, "hgf"),
     ("one-row", 67, 1, 3, 2, 3, 3, 0.05, "hgf"),
     ("one-pixel", 1, 1, 3, 2, 4, 2, 0.05, "hgf"),
+    # degenerate frames on the default kernels: a single column (W % 4 != 0: repacked k_coef5 rows), and 40 labels on
+    # one pixel / one column / a 3 x 2 frame (k_agg6's label split over a single tile)
+    ("one-column", 1, 67, 3, 2, 3, 3, 0.05, "hgf"),
+    ("one-pixel-L40", 1, 1, 3, 2, 40, 9, 0.05, "hgf"),
+    ("one-column-L40", 1, 45, 3, 2, 40, 9, 0.05, "gf"),
+    ("3x2-L40", 3, 2, 3, 2, 40, 9, 0.05, "hgf"),
     ("L1", 33, 35, 3, 2, 1, 9, 0.05, "hgf"),
     # label-interleaved k_coef3 -> k_agg3 path: two strips + a partial 16-pixel group, a partial 32-label batch
     ("il-n6-L35", 100, 37, 3, 2, 35, 9, 0.05, "hgf"),
