@@ -550,6 +550,49 @@ hgf_status slices(hgf_ctx* h, const float* guide, const float* vol, int L, int l
                      [](int, int, const float**) { return cudaSuccess; });
 }
 
+// The fused single-slice pass (one slice, few-label mode on): guidance, then the statistics pass that also sums the
+// slice's cost products and writes its coefficients (no statistics in HBM, no coefficient kernel), then the planar
+// aggregation with the requested outputs.  Returns false (nothing enqueued) where it does not apply.
+bool fused_single_ok(hgf_ctx* h) {
+  const char* fe = std::getenv("HGF_FILTER_FUSED");
+  const hgf::WLayout& wl = h->planar_now ? h->wlay_planar : h->wlay;
+  return !wl.il && !(fe && fe[0] == '0') && h->n <= hgf::kStats4MaxN && 64 + 2 * h->r <= 128 &&
+         hgf::stats4_smem(h->n, h->r, 1) <= 200 * 1024;
+}
+
+hgf_status fused_single(hgf_ctx* h, const float* guide, const float* src, int label_offset, float* filtered_out,
+                        int do_wta, int32_t* labels_out, float* min_cost_out, int64_t* keys_out) {
+  const hgf::WLayout& wl = h->planar_now ? h->wlay_planar : h->wlay;
+  cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
+    return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->gp_pitch, h->m, h->d, h->W, h->H, h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
+  e = traced(h, HGF_KC_STATS, h->stream, [&] {
+    const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
+    return hgf::launch_filter1(h->n, h->G, src, h->wbuf, wl, h->W, h->H, h->r, h->eps, h->mode, lam0, h->stream);
+  });
+  if (e != cudaSuccess) return cuda_fail(h, e, "fused statistics + coefficients");
+  hgf::AggArgs a{};
+  a.G = h->G;
+  a.wbuf = h->wbuf;
+  a.W = h->W; a.H = h->H; a.r = h->r; a.L = 1; a.pad = wl.pad; a.il = 0;
+  a.label_base = label_offset;
+  a.filtered_out = filtered_out;
+  a.do_wta = do_wta;
+  a.first = 1;
+  a.last = 1;
+  a.best_cost = h->best_cost;
+  a.best_label = h->best_label;
+  a.labels_out = labels_out;
+  a.min_cost_out = min_cost_out;
+  a.keys_out = keys_out;
+  a.peer_keys = h->peer_keys;
+  a.rows_per_owner = h->rows_per_owner;
+  e = launch_agg_chunk(h, a);
+  if (e != cudaSuccess) return cuda_fail(h, e, "agg");
+  return HGF_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -776,35 +819,7 @@ hgf_status hgf_filter(hgf_handle h, const float* guide, const float* src, float*
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   SmallLMode sm(h, 1);
-  const char* fe = std::getenv("HGF_FILTER_FUSED");
-  const hgf::WLayout& wl = h->planar_now ? h->wlay_planar : h->wlay;
-  if (!wl.il && !(fe && fe[0] == '0') && h->n <= hgf::kStats4MaxN && 64 + 2 * h->r <= 128 &&
-      hgf::stats4_smem(h->n, h->r, 1) <= 200 * 1024) {
-    // one slice: the statistics pass also sums the slice's cost products and writes its coefficients (no
-    // statistics in HBM, no coefficient kernel), then the planar aggregation
-    cudaError_t e = traced(h, HGF_KC_GUIDANCE, h->stream, [&] {
-      return hgf::launch_poly_guidance(guide, h->G, h->Gp, h->gp_pitch, h->m, h->d, h->W, h->H, h->stream);
-    });
-    if (e != cudaSuccess) return cuda_fail(h, e, "poly_guidance");
-    e = traced(h, HGF_KC_STATS, h->stream, [&] {
-      const float lam0 = (h->mode == HGF_MODE_HGF) ? (float)h->eps : 0.0f;
-      return hgf::launch_filter1(h->n, h->G, src, h->wbuf, wl, h->W, h->H, h->r, h->eps, h->mode, lam0, h->stream);
-    });
-    if (e != cudaSuccess) return cuda_fail(h, e, "fused statistics + coefficients");
-    hgf::AggArgs a{};
-    a.G = h->G;
-    a.wbuf = h->wbuf;
-    a.W = h->W; a.H = h->H; a.r = h->r; a.L = 1; a.pad = wl.pad; a.il = 0;
-    a.label_base = 0;
-    a.filtered_out = dst;
-    a.first = 1;
-    a.last = 1;
-    a.best_cost = h->best_cost;
-    a.best_label = h->best_label;
-    e = launch_agg_chunk(h, a);
-    if (e != cudaSuccess) return cuda_fail(h, e, "agg");
-    return HGF_OK;
-  }
+  if (fused_single_ok(h)) return fused_single(h, guide, src, 0, dst, 0, nullptr, nullptr, nullptr);
   if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   return slices(h, guide, src, 1, 0, dst, 0, nullptr, nullptr, nullptr);
 }
@@ -824,8 +839,11 @@ hgf_status hgf_aggregate_wta_ex(hgf_handle h, const float* guide, const float* c
   hgf_status s = check_async(h);
   if (s != HGF_OK) return s;
   SmallLMode sm(h, L);
-  if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   const int do_wta = (labels_out || min_cost_out || keys_out) ? 1 : 0;
+  // one slice: the fused single-slice pass (as hgf_filter), the WTA over the one label in its aggregation
+  if (L == 1 && fused_single_ok(h))
+    return fused_single(h, guide, cost_volume, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
+  if ((s = frame_stats(h, guide, 0, h->H)) != HGF_OK) return s;
   return slices(h, guide, cost_volume, L, label_offset, filtered_out, do_wta, labels_out, min_cost_out, keys_out);
 }
 
